@@ -1,0 +1,761 @@
+// abi.cu — the extern "C" surface declared in include/slab_b200.h. Every entry point
+// translates internal exceptions into status codes; argument checks precede any work.
+#include <cstring>
+#include <new>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+using namespace slabgpu;
+
+namespace {
+
+	thread_local std::string t_last_error;
+
+	template< class F >
+	int guarded( F && f ) {
+		try {
+			f();
+			return SLAB_OK;
+		} catch( const Error & e ) {
+			t_last_error = e.message;
+			return e.status;
+		} catch( const std::bad_alloc & ) {
+			t_last_error = "host allocation failed";
+			return SLAB_ERR_INTERNAL;
+		} catch( const std::exception & e ) {
+			t_last_error = e.what();
+			return SLAB_ERR_INTERNAL;
+		}
+	}
+
+	void need( const void * p, const char * what ) {
+		if( p == nullptr ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, std::string( what ) + ": null handle or pointer" );
+		}
+	}
+
+	void same_ctx( const slab_ctx_s * a, const slab_ctx_s * b ) {
+		if( a != b ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "operands belong to different contexts" );
+		}
+	}
+
+	void bind( slab_ctx_s * ctx ) {
+		SLAB_CUDA( cudaSetDevice( ctx->device ) );
+	}
+
+} // namespace
+
+extern "C" {
+
+int slab_abi_version( void ) {
+	return SLAB_B200_ABI_VERSION;
+}
+
+const char * slab_last_error( void ) {
+	return t_last_error.c_str();
+}
+
+const char * slab_status_name( int status ) {
+	switch( status ) {
+		case SLAB_OK: return "ok";
+		case SLAB_ERR_DIMENSION_MISMATCH: return "DimensionMismatch";
+		case SLAB_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+		case SLAB_ERR_SOLVER_BREAKDOWN: return "SolverBreakdown";
+		case SLAB_ERR_CUDA: return "CudaError";
+		default: return "InternalError";
+	}
+}
+
+uint64_t slab_launch_count( void ) {
+	return g_launch_count;
+}
+
+// ---------------------------------------------------------------- context
+
+int slab_ctx_create( int device, slab_ctx_t * out ) {
+	return guarded( [ & ] {
+		need( out, "slab_ctx_create" );
+		*out = nullptr;
+		int count = 0;
+		const cudaError_t err = cudaGetDeviceCount( &count );
+		if( err != cudaSuccess || count == 0 ) {
+			fail( SLAB_ERR_CUDA, std::string( "no CUDA device available (there is no CPU fallback): " )
+				+ cudaGetErrorString( err ) );
+		}
+		if( device < 0 || device >= count ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "device index out of range" );
+		}
+		SLAB_CUDA( cudaSetDevice( device ) );
+		cudaDeviceProp prop{};
+		SLAB_CUDA( cudaGetDeviceProperties( &prop, device ) );
+		if( prop.major < 10 ) {
+			fail( SLAB_ERR_CUDA, std::string( "device " ) + prop.name + " is sm_" + std::to_string( prop.major )
+				+ std::to_string( prop.minor ) + "; this library is built for sm_100a only" );
+		}
+		std::unique_ptr< slab_ctx_s > ctx( new slab_ctx_s );
+		ctx->device = device;
+		ctx->sm_count = prop.multiProcessorCount;
+		ctx->cc_major = prop.major;
+		ctx->cc_minor = prop.minor;
+		ctx->hbm_bytes = prop.totalGlobalMem;
+		SLAB_CUDA( cudaStreamCreateWithFlags( &ctx->stream, cudaStreamNonBlocking ) );
+		SLAB_CUDA( cudaMalloc( &ctx->d_scalars, S_COUNT * sizeof( double ) ) );
+		SLAB_CUDA( cudaMemset( ctx->d_scalars, 0, S_COUNT * sizeof( double ) ) );
+		SLAB_CUDA( cudaMalloc( &ctx->d_counter, sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaMemset( ctx->d_counter, 0, sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaEventCreate( &ctx->timer_start ) );
+		SLAB_CUDA( cudaEventCreate( &ctx->timer_stop ) );
+		ensure_partials( ctx.get(), 4096 );
+		ensure_pinned( ctx.get(), 1024 );
+		*out = ctx.release();
+	} );
+}
+
+int slab_ctx_destroy( slab_ctx_t ctx ) {
+	return guarded( [ & ] {
+		if( ctx == nullptr ) {
+			return;
+		}
+		cudaSetDevice( ctx->device );
+		cudaStreamSynchronize( ctx->stream );
+		cudaFree( ctx->d_scalars );
+		cudaFree( ctx->d_partials );
+		cudaFree( ctx->d_counter );
+		if( ctx->h_pinned ) cudaFreeHost( ctx->h_pinned );
+		cudaEventDestroy( ctx->timer_start );
+		cudaEventDestroy( ctx->timer_stop );
+		cudaStreamDestroy( ctx->stream );
+		delete ctx;
+	} );
+}
+
+int slab_ctx_sync( slab_ctx_t ctx ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_sync" );
+		bind( ctx );
+		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+	} );
+}
+
+int slab_ctx_set_dot_mode( slab_ctx_t ctx, int mode ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_set_dot_mode" );
+		if( mode != SLAB_DOT_EXACT && mode != SLAB_DOT_TREE ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "unknown dot mode" );
+		}
+		ctx->dot_mode = mode;
+	} );
+}
+
+int slab_ctx_get_dot_mode( slab_ctx_t ctx, int * mode ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_get_dot_mode" );
+		need( mode, "slab_ctx_get_dot_mode" );
+		*mode = ctx->dot_mode;
+	} );
+}
+
+int slab_ctx_set_graphs( slab_ctx_t ctx, int enabled ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_set_graphs" );
+		ctx->use_graphs = enabled ? 1 : 0;
+	} );
+}
+
+int slab_ctx_set_fused_transfers( slab_ctx_t ctx, int enabled ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_set_fused_transfers" );
+		ctx->fused_transfers = enabled ? 1 : 0;
+	} );
+}
+
+int slab_ctx_timer_start( slab_ctx_t ctx ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_timer_start" );
+		bind( ctx );
+		SLAB_CUDA( cudaEventRecord( ctx->timer_start, ctx->stream ) );
+	} );
+}
+
+int slab_ctx_timer_stop( slab_ctx_t ctx, double * elapsed_ms ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_timer_stop" );
+		need( elapsed_ms, "slab_ctx_timer_stop" );
+		bind( ctx );
+		SLAB_CUDA( cudaEventRecord( ctx->timer_stop, ctx->stream ) );
+		SLAB_CUDA( cudaEventSynchronize( ctx->timer_stop ) );
+		float ms = 0.0f;
+		SLAB_CUDA( cudaEventElapsedTime( &ms, ctx->timer_start, ctx->timer_stop ) );
+		*elapsed_ms = ms;
+	} );
+}
+
+int slab_ctx_device_info( slab_ctx_t ctx, int * sm_count, int * cc_major, int * cc_minor, uint64_t * hbm_bytes ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_device_info" );
+		if( sm_count ) *sm_count = ctx->sm_count;
+		if( cc_major ) *cc_major = ctx->cc_major;
+		if( cc_minor ) *cc_minor = ctx->cc_minor;
+		if( hbm_bytes ) *hbm_bytes = ctx->hbm_bytes;
+	} );
+}
+
+// ---------------------------------------------------------------- vectors
+
+int slab_vec_create( slab_ctx_t ctx, uint64_t n, double value, slab_vec_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_vec_create" );
+		need( out, "slab_vec_create" );
+		*out = nullptr;
+		bind( ctx );
+		*out = vec_new( ctx, n, value );
+	} );
+}
+
+int slab_vec_destroy( slab_vec_t v ) {
+	return guarded( [ & ] {
+		if( v ) {
+			cudaSetDevice( v->ctx->device );
+			cudaStreamSynchronize( v->ctx->stream );
+			vec_free( v );
+		}
+	} );
+}
+
+int slab_vec_size( slab_vec_t v, uint64_t * n ) {
+	return guarded( [ & ] {
+		need( v, "slab_vec_size" );
+		need( n, "slab_vec_size" );
+		*n = v->n;
+	} );
+}
+
+int slab_vec_upload( slab_vec_t v, const double * host, uint64_t n ) {
+	return guarded( [ & ] {
+		need( v, "slab_vec_upload" );
+		if( n != v->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "upload: host length differs from the vector length" );
+		}
+		if( n == 0 ) {
+			return;
+		}
+		need( host, "slab_vec_upload" );
+		bind( v->ctx );
+		SLAB_CUDA( cudaMemcpyAsync( v->d, host, n * sizeof( double ), cudaMemcpyHostToDevice, v->ctx->stream ) );
+		SLAB_CUDA( cudaStreamSynchronize( v->ctx->stream ) );
+	} );
+}
+
+int slab_vec_download( slab_vec_t v, double * host, uint64_t n ) {
+	return guarded( [ & ] {
+		need( v, "slab_vec_download" );
+		if( n != v->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "download: host length differs from the vector length" );
+		}
+		if( n == 0 ) {
+			return;
+		}
+		need( host, "slab_vec_download" );
+		bind( v->ctx );
+		SLAB_CUDA( cudaMemcpyAsync( host, v->d, n * sizeof( double ), cudaMemcpyDeviceToHost, v->ctx->stream ) );
+		SLAB_CUDA( cudaStreamSynchronize( v->ctx->stream ) );
+	} );
+}
+
+int slab_vec_copy( slab_vec_t dst, slab_vec_t src ) {
+	return guarded( [ & ] {
+		need( dst, "slab_vec_copy" );
+		need( src, "slab_vec_copy" );
+		same_ctx( dst->ctx, src->ctx );
+		if( dst->n != src->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "copy: vector lengths differ" );
+		}
+		bind( dst->ctx );
+		if( dst->d != src->d && dst->n > 0 ) {
+			SLAB_CUDA( cudaMemcpyAsync( dst->d, src->d, dst->n * sizeof( double ), cudaMemcpyDeviceToDevice,
+				dst->ctx->stream ) );
+		}
+	} );
+}
+
+// rng.hpp:35-65 — the sequence is inherently serial, so it is generated on the host and uploaded
+int slab_vec_fill_lcg( slab_vec_t v, uint64_t seed, uint64_t * state_out ) {
+	return guarded( [ & ] {
+		need( v, "slab_vec_fill_lcg" );
+		bind( v->ctx );
+		std::vector< double > host( v->n );
+		uint64_t state = seed;
+		for( uint64_t i = 0; i < v->n; ++i ) {
+			state = state * 6364136223846793005ULL + 1442695040888963407ULL;
+			const double unit = static_cast< double >( state >> 11 ) * 0x1.0p-53;
+			host[ i ] = 2.0 * unit - 1.0;
+		}
+		if( v->n > 0 ) {
+			SLAB_CUDA( cudaMemcpyAsync( v->d, host.data(), v->n * sizeof( double ), cudaMemcpyHostToDevice,
+				v->ctx->stream ) );
+			SLAB_CUDA( cudaStreamSynchronize( v->ctx->stream ) );
+		}
+		if( state_out ) {
+			*state_out = state;
+		}
+	} );
+}
+
+int slab_set_all( slab_vec_t v, double value ) {
+	return guarded( [ & ] {
+		need( v, "set_all" );
+		bind( v->ctx );
+		op_set_all( v, value );
+	} );
+}
+
+int slab_dot( slab_vec_t x, slab_vec_t y, double * out ) {
+	return guarded( [ & ] {
+		need( x, "dot" );
+		need( y, "dot" );
+		need( out, "dot" );
+		same_ctx( x->ctx, y->ctx );
+		bind( x->ctx );
+		*out = op_dot( x, y );
+	} );
+}
+
+int slab_waxpby( slab_vec_t w, double alpha, slab_vec_t x, double beta, slab_vec_t y ) {
+	return guarded( [ & ] {
+		need( w, "waxpby" );
+		need( x, "waxpby" );
+		need( y, "waxpby" );
+		same_ctx( w->ctx, x->ctx );
+		same_ctx( w->ctx, y->ctx );
+		bind( w->ctx );
+		op_waxpby( w, alpha, x, beta, y );
+	} );
+}
+
+// ---------------------------------------------------------------- matrices
+
+int slab_mat_create_csr( slab_ctx_t ctx, uint64_t nrows, uint64_t ncols, const uint64_t * row_offsets,
+	const uint64_t * col_indices, const double * values, slab_mat_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_mat_create_csr" );
+		need( out, "slab_mat_create_csr" );
+		*out = nullptr;
+		need( row_offsets, "slab_mat_create_csr" );
+		if( row_offsets[ nrows ] > 0 ) {
+			need( col_indices, "slab_mat_create_csr" );
+			need( values, "slab_mat_create_csr" );
+		}
+		bind( ctx );
+		*out = mat_from_csr( ctx, nrows, ncols, row_offsets, col_indices, values, true );
+	} );
+}
+
+int slab_mat_create_stencil27( slab_ctx_t ctx, uint64_t nx, uint64_t ny, uint64_t nz, slab_mat_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_mat_create_stencil27" );
+		need( out, "slab_mat_create_stencil27" );
+		*out = nullptr;
+		bind( ctx );
+		*out = mat_stencil27( ctx, nx, ny, nz );
+	} );
+}
+
+int slab_mat_create_restriction( slab_ctx_t ctx, uint64_t nx, uint64_t ny, uint64_t nz, slab_mat_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_mat_create_restriction" );
+		need( out, "slab_mat_create_restriction" );
+		*out = nullptr;
+		bind( ctx );
+		*out = mat_restriction( ctx, nx, ny, nz );
+	} );
+}
+
+int slab_mat_destroy( slab_mat_t A ) {
+	return guarded( [ & ] {
+		if( A ) {
+			cudaSetDevice( A->ctx->device );
+			cudaStreamSynchronize( A->ctx->stream );
+			delete A;
+		}
+	} );
+}
+
+int slab_mat_shape( slab_mat_t A, uint64_t * nrows, uint64_t * ncols, uint64_t * nnz ) {
+	return guarded( [ & ] {
+		need( A, "slab_mat_shape" );
+		if( nrows ) *nrows = A->nrows;
+		if( ncols ) *ncols = A->ncols;
+		if( nnz ) *nnz = A->nnz;
+	} );
+}
+
+int slab_mat_download_csr( slab_mat_t A, uint64_t * row_offsets, uint64_t * col_indices, double * values ) {
+	return guarded( [ & ] {
+		need( A, "slab_mat_download_csr" );
+		need( row_offsets, "slab_mat_download_csr" );
+		if( A->nnz > 0 ) {
+			need( col_indices, "slab_mat_download_csr" );
+			need( values, "slab_mat_download_csr" );
+		}
+		bind( A->ctx );
+		mat_download_csr( A, row_offsets, col_indices, values );
+	} );
+}
+
+int slab_mat_device_bytes( slab_mat_t A, uint64_t * bytes ) {
+	return guarded( [ & ] {
+		need( A, "slab_mat_device_bytes" );
+		need( bytes, "slab_mat_device_bytes" );
+		*bytes = A->sell.bytes() + ( A->transposed ? A->transposed->sell.bytes() : 0 );
+	} );
+}
+
+// ---------------------------------------------------------------- masks
+
+int slab_mask_create( slab_ctx_t ctx, uint64_t universe, const uint64_t * members, uint64_t count, slab_mask_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_mask_create" );
+		need( out, "slab_mask_create" );
+		*out = nullptr;
+		if( count > 0 ) {
+			need( members, "slab_mask_create" );
+		}
+		if( universe >= ( uint64_t( 1 ) << 31 ) ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "IndexMask: universe too large for one device" );
+		}
+		std::vector< int32_t > m32( count );
+		for( uint64_t k = 0; k < count; ++k ) { // index_mask.hpp:41-48
+			if( members[ k ] >= universe ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, "IndexMask: member out of range" );
+			}
+			if( k > 0 && members[ k ] <= members[ k - 1 ] ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, "IndexMask: members must be strictly increasing" );
+			}
+			m32[ k ] = static_cast< int32_t >( members[ k ] );
+		}
+		bind( ctx );
+		std::unique_ptr< slab_mask_s > m( new slab_mask_s );
+		m->ctx = ctx;
+		m->universe = universe;
+		m->count = count;
+		SLAB_CUDA( cudaMalloc( &m->d_members, std::max< uint64_t >( count, 1 ) * sizeof( int32_t ) ) );
+		if( count > 0 ) {
+			SLAB_CUDA( cudaMemcpy( m->d_members, m32.data(), count * sizeof( int32_t ), cudaMemcpyHostToDevice ) );
+		}
+		*out = m.release();
+	} );
+}
+
+int slab_mask_destroy( slab_mask_t m ) {
+	return guarded( [ & ] {
+		if( m ) {
+			cudaSetDevice( m->ctx->device );
+			cudaStreamSynchronize( m->ctx->stream );
+			delete m;
+		}
+	} );
+}
+
+int slab_mask_info( slab_mask_t m, uint64_t * universe, uint64_t * count ) {
+	return guarded( [ & ] {
+		need( m, "slab_mask_info" );
+		if( universe ) *universe = m->universe;
+		if( count ) *count = m->count;
+	} );
+}
+
+int slab_mxv( slab_vec_t y, slab_mat_t A, slab_vec_t x, unsigned desc ) {
+	return guarded( [ & ] {
+		need( y, "mxv" );
+		need( A, "mxv" );
+		need( x, "mxv" );
+		same_ctx( A->ctx, y->ctx );
+		same_ctx( A->ctx, x->ctx );
+		bind( A->ctx );
+		op_mxv( y, nullptr, A, x, desc );
+	} );
+}
+
+int slab_mxv_masked( slab_vec_t y, slab_mask_t mask, slab_mat_t A, slab_vec_t x, unsigned desc ) {
+	return guarded( [ & ] {
+		need( y, "mxv" );
+		need( mask, "mxv" );
+		need( A, "mxv" );
+		need( x, "mxv" );
+		same_ctx( A->ctx, y->ctx );
+		same_ctx( A->ctx, x->ctx );
+		same_ctx( A->ctx, mask->ctx );
+		bind( A->ctx );
+		op_mxv( y, mask, A, x, desc );
+	} );
+}
+
+// ---------------------------------------------------------------- levels
+
+int slab_hierarchy_create( slab_ctx_t ctx, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t levels, slab_level_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "build_hierarchy" );
+		need( out, "build_hierarchy" );
+		*out = nullptr;
+		bind( ctx );
+		*out = hierarchy_create( ctx, nx, ny, nz, levels );
+	} );
+}
+
+int slab_level_create_csr( slab_ctx_t ctx, uint64_t n, const uint64_t * row_offsets, const uint64_t * col_indices,
+	const double * values, slab_level_t * out ) {
+	return guarded( [ & ] {
+		need( ctx, "ProblemLevel" );
+		need( out, "ProblemLevel" );
+		*out = nullptr;
+		need( row_offsets, "ProblemLevel" );
+		bind( ctx );
+		*out = level_from_csr( ctx, n, row_offsets, col_indices, values );
+	} );
+}
+
+int slab_level_destroy( slab_level_t level ) {
+	return guarded( [ & ] {
+		if( level ) {
+			cudaSetDevice( level->ctx->device );
+			cudaStreamSynchronize( level->ctx->stream );
+			delete level;
+		}
+	} );
+}
+
+int slab_level_coarser( slab_level_t level, slab_level_t * out ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_coarser" );
+		need( out, "slab_level_coarser" );
+		*out = level->coarser.get();
+	} );
+}
+
+int slab_level_matrix( slab_level_t level, slab_mat_t * A ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_matrix" );
+		need( A, "slab_level_matrix" );
+		*A = level->A.get();
+	} );
+}
+
+int slab_level_restriction( slab_level_t level, slab_mat_t * R ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_restriction" );
+		need( R, "slab_level_restriction" );
+		*R = level->R.get();
+	} );
+}
+
+int slab_level_diag( slab_level_t level, slab_vec_t * a_diag ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_diag" );
+		need( a_diag, "slab_level_diag" );
+		*a_diag = level->a_diag.get();
+	} );
+}
+
+int slab_level_info( slab_level_t level, uint64_t dims[ 3 ], uint64_t * n, uint64_t * nnz, uint64_t * num_colors,
+	uint64_t * depth ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_info" );
+		if( dims ) {
+			std::memcpy( dims, level->dims, sizeof( level->dims ) );
+		}
+		if( n ) *n = level->n;
+		if( nnz ) *nnz = level->nnz;
+		if( num_colors ) *num_colors = level->num_colors;
+		if( depth ) {
+			uint64_t d = 0;
+			for( slab_level_s * at = level; at; at = at->coarser.get() ) {
+				++d;
+			}
+			*depth = d;
+		}
+	} );
+}
+
+int slab_level_color_info( slab_level_t level, uint64_t k, uint64_t * size, uint64_t * color_nnz ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_color_info" );
+		if( k >= level->num_colors ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "colour index out of range" );
+		}
+		if( size ) *size = level->color_size[ k ];
+		if( color_nnz ) *color_nnz = level->color_nnz[ k ];
+	} );
+}
+
+int slab_level_color_members( slab_level_t level, uint64_t k, uint64_t * members ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_color_members" );
+		if( k >= level->num_colors ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "colour index out of range" );
+		}
+		const uint64_t size = level->color_size[ k ];
+		if( size == 0 ) {
+			return;
+		}
+		need( members, "slab_level_color_members" );
+		bind( level->ctx );
+		std::vector< int32_t > rows( size );
+		SLAB_CUDA( cudaMemcpy( rows.data(), level->d_rows + level->color_pos[ k ], size * sizeof( int32_t ),
+			cudaMemcpyDeviceToHost ) );
+		for( uint64_t q = 0; q < size; ++q ) {
+			members[ q ] = static_cast< uint64_t >( rows[ q ] );
+		}
+	} );
+}
+
+int slab_level_stats_get( slab_level_t level, slab_level_stats * out ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_stats_get" );
+		need( out, "slab_level_stats_get" );
+		*out = level->stats;
+	} );
+}
+
+int slab_level_stats_reset( slab_level_t level ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_stats_reset" );
+		for( slab_level_s * at = level; at; at = at->coarser.get() ) {
+			at->stats = slab_level_stats{};
+		}
+	} );
+}
+
+// ---------------------------------------------------------------- smoother / multigrid
+
+#define SLAB_LEVEL_ZR( name )                  \
+	need( level, name );                       \
+	need( z, name );                           \
+	need( r, name );                           \
+	same_ctx( level->ctx, z->ctx );            \
+	same_ctx( level->ctx, r->ctx );            \
+	bind( level->ctx )
+
+int slab_rbgs_color_step( slab_level_t level, uint64_t k, slab_vec_t z, slab_vec_t r ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "rbgs_color_step" );
+		rbgs_color_step( level, k, z, r );
+	} );
+}
+
+int slab_rbgs_forward( slab_level_t level, slab_vec_t z, slab_vec_t r ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "rbgs_forward" );
+		rbgs_forward( level, z, r );
+	} );
+}
+
+int slab_rbgs_backward( slab_level_t level, slab_vec_t z, slab_vec_t r ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "rbgs_backward" );
+		rbgs_backward( level, z, r );
+	} );
+}
+
+int slab_rbgs_symmetric( slab_level_t level, slab_vec_t z, slab_vec_t r, uint64_t sweeps ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "rbgs_symmetric" );
+		rbgs_symmetric( level, z, r, sweeps );
+	} );
+}
+
+int slab_restrict_vector( slab_level_t level, slab_vec_t v_fine, slab_vec_t out ) {
+	return guarded( [ & ] {
+		need( level, "restrict_vector" );
+		need( v_fine, "restrict_vector" );
+		need( out, "restrict_vector" );
+		same_ctx( level->ctx, v_fine->ctx );
+		same_ctx( level->ctx, out->ctx );
+		bind( level->ctx );
+		restrict_vector( level, v_fine, out );
+	} );
+}
+
+int slab_refine_and_add( slab_level_t level, slab_vec_t z, slab_vec_t z_c ) {
+	return guarded( [ & ] {
+		need( level, "refine_and_add" );
+		need( z, "refine_and_add" );
+		need( z_c, "refine_and_add" );
+		same_ctx( level->ctx, z->ctx );
+		same_ctx( level->ctx, z_c->ctx );
+		bind( level->ctx );
+		refine_and_add( level, z, z_c );
+	} );
+}
+
+int slab_mg_vcycle( slab_level_t level, slab_vec_t z, slab_vec_t r, uint64_t sweeps ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "mg_vcycle" );
+		mg_vcycle( level, z, r, sweeps );
+	} );
+}
+
+// ---------------------------------------------------------------- cg
+
+void slab_cg_config_default( slab_cg_config * cfg ) {
+	if( cfg ) {
+		cfg->max_iters = 500;
+		cfg->rtol = 1e-6;
+		cfg->use_preconditioner = 1;
+		cfg->has_fixed_iterations = 0;
+		cfg->fixed_iterations = 0;
+		cfg->sweeps = 1;
+	}
+}
+
+int slab_cg_solve( slab_level_t hierarchy, slab_vec_t b, slab_vec_t x0, const slab_cg_config * cfg, slab_vec_t x,
+	double * history, slab_cg_result * result ) {
+	return guarded( [ & ] {
+		need( hierarchy, "cg_solve" );
+		need( b, "cg_solve" );
+		need( x0, "cg_solve" );
+		need( x, "cg_solve" );
+		need( cfg, "cg_solve" );
+		need( history, "cg_solve" );
+		same_ctx( hierarchy->ctx, b->ctx );
+		same_ctx( hierarchy->ctx, x0->ctx );
+		same_ctx( hierarchy->ctx, x->ctx );
+		bind( hierarchy->ctx );
+		cg_solve( hierarchy, b, x0, cfg, x, history, result );
+	} );
+}
+
+int slab_cg_solve_host( slab_level_t hierarchy, const double * b, const double * x0, uint64_t n,
+	const slab_cg_config * cfg, double * x, double * history, slab_cg_result * result ) {
+	return guarded( [ & ] {
+		need( hierarchy, "cg_solve" );
+		need( cfg, "cg_solve" );
+		need( history, "cg_solve" );
+		if( n != hierarchy->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "cg_solve: vector lengths differ from the system size" );
+		}
+		if( n > 0 ) {
+			need( b, "cg_solve" );
+			need( x0, "cg_solve" );
+			need( x, "cg_solve" );
+		}
+		bind( hierarchy->ctx );
+		cg_solve_host( hierarchy, b, x0, cfg, x, history, result );
+	} );
+}
+
+int slab_residual_norm( slab_mat_t A, slab_vec_t x, slab_vec_t b, double * out ) {
+	return guarded( [ & ] {
+		need( A, "residual_norm" );
+		need( x, "residual_norm" );
+		need( b, "residual_norm" );
+		need( out, "residual_norm" );
+		same_ctx( A->ctx, x->ctx );
+		same_ctx( A->ctx, b->ctx );
+		bind( A->ctx );
+		*out = residual_norm( A, x, b );
+	} );
+}
+
+} // extern "C"

@@ -1,0 +1,280 @@
+// cg.cu — preconditioned conjugate gradients (cg.hpp:77-142) driving the device kernels.
+//
+// The three scalars per iteration (rho, p'Ap, r'r) never leave the device in fixed-iteration
+// runs: the dot kernels write them into ctx->d_scalars, the vector updates divide them on the
+// device with IEEE division (bit-identical to the host's), and one CUDA graph per iteration is
+// replayed without host synchronisation. The residual history and the breakdown test
+// (cg.hpp:124-126) are evaluated on the host from the recorded scalars.
+#include <algorithm>
+#include <cmath>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace slabgpu {
+
+	CgWorkspace::~CgWorkspace() {
+		if( d_hist_rr ) cudaFree( d_hist_rr );
+		if( d_hist_pq ) cudaFree( d_hist_pq );
+		if( d_iter ) cudaFree( d_iter );
+		if( iter_exec ) cudaGraphExecDestroy( iter_exec );
+	}
+
+	namespace {
+
+		CgWorkspace * workspace( slab_level_s * H, uint64_t iterations ) {
+			slab_ctx_s * ctx = H->ctx;
+			if( !H->cg ) {
+				H->cg.reset( new CgWorkspace );
+				H->cg->r.reset( vec_new( ctx, H->n, 0.0 ) );
+				H->cg->z.reset( vec_new( ctx, H->n, 0.0 ) );
+				H->cg->p.reset( vec_new( ctx, H->n, 0.0 ) );
+				H->cg->q.reset( vec_new( ctx, H->n, 0.0 ) );
+				SLAB_CUDA( cudaMalloc( &H->cg->d_iter, sizeof( unsigned int ) ) );
+			}
+			CgWorkspace * ws = H->cg.get();
+			if( iterations + 1 > ws->hist_cap ) {
+				SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+				if( ws->d_hist_rr ) cudaFree( ws->d_hist_rr );
+				if( ws->d_hist_pq ) cudaFree( ws->d_hist_pq );
+				ws->d_hist_rr = ws->d_hist_pq = nullptr;
+				ws->hist_cap = std::max< uint64_t >( iterations + 1, 64 );
+				SLAB_CUDA( cudaMalloc( &ws->d_hist_rr, ws->hist_cap * sizeof( double ) ) );
+				SLAB_CUDA( cudaMalloc( &ws->d_hist_pq, ws->hist_cap * sizeof( double ) ) );
+				if( ws->iter_exec ) { // the graph holds the old history pointers
+					cudaGraphExecDestroy( ws->iter_exec );
+					ws->iter_exec = nullptr;
+				}
+			}
+			return ws;
+		}
+
+		// one CG iteration, cg.hpp:110-132, enqueue only
+		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg ) {
+			slab_ctx_s * ctx = H->ctx;
+			cudaStream_t st = ctx->stream;
+			slab_vec_s * r = ws->r.get();
+			slab_vec_s * z = ws->z.get();
+			slab_vec_s * p = ws->p.get();
+			slab_vec_s * q = ws->q.get();
+			if( cfg->use_preconditioner ) {
+				op_set_all( z, 0.0 ); // cg.hpp:111
+				mg_vcycle_enqueue( H, z, r, cfg->sweeps, false );
+			} else {
+				op_waxpby( z, 1.0, r, 0.0, r ); // cg.hpp:114
+			}
+			op_dot_to_slot( r, z, S_RHO );                                        // cg.hpp:116
+			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
+			op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
+			op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
+			kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
+			op_dot_to_slot( r, r, S_RR );                                         // cg.hpp:132
+			kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
+		}
+
+		void vcycle_stats_all( slab_level_s * L, uint64_t sweeps ) {
+			for( ; L != nullptr; L = L->coarser.get() ) {
+				if( L->coarser ) {
+					L->stats.nnz_visited += 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz;
+				} else {
+					L->stats.nnz_visited += 2 * sweeps * L->nnz;
+				}
+			}
+		}
+
+	} // namespace
+
+	void cg_solve( slab_level_s * H, slab_vec_s * b, slab_vec_s * x0, const slab_cg_config * cfg, slab_vec_s * x,
+		double * history, slab_cg_result * result ) {
+		if( !( cfg->rtol > 0.0 ) ) { // cg.hpp:79-81
+			fail( SLAB_ERR_INVALID_ARGUMENT, "CGConfig: rtol must be positive" );
+		}
+		if( cfg->max_iters < 1 ) { // cg.hpp:82-84
+			fail( SLAB_ERR_INVALID_ARGUMENT, "CGConfig: max_iters must be at least 1" );
+		}
+		if( cfg->use_preconditioner && cfg->sweeps < 1 ) { // smoother.hpp:105-107, reached through mg_vcycle
+			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
+		}
+		const uint64_t n = H->n;
+		if( b->n != n || x0->n != n || x->n != n ) { // cg.hpp:86-88
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "cg_solve: vector lengths differ from the system size" );
+		}
+		if( x == b || x->d == b->d ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "cg_solve: the solution vector must not alias b" );
+		}
+		slab_ctx_s * ctx = H->ctx;
+		cudaStream_t st = ctx->stream;
+		const bool fixed = cfg->has_fixed_iterations != 0;
+		const uint64_t planned = fixed ? std::min( cfg->fixed_iterations, cfg->max_iters ) : cfg->max_iters;
+		CgWorkspace * ws = workspace( H, planned );
+		slab_vec_s * r = ws->r.get();
+
+		SLAB_CUDA( cudaEventRecord( ctx->timer_start, st ) );
+		if( x->d != x0->d ) { // out.solution = x0, cg.hpp:91
+			SLAB_CUDA( cudaMemcpyAsync( x->d, x0->d, n * sizeof( double ), cudaMemcpyDeviceToDevice, st ) );
+		}
+		op_mxv( r, nullptr, H->A.get(), x, SLAB_DESC_NONE ); // cg.hpp:95
+		op_waxpby( r, 1.0, b, -1.0, r );                     // cg.hpp:96
+		op_dot_to_slot( b, b, S_BB );                        // cg.hpp:98
+		op_dot_to_slot( r, r, S_RR );                        // cg.hpp:100
+		SLAB_CUDA( cudaMemsetAsync( ws->d_iter, 0, sizeof( unsigned int ), st ) );
+		ensure_pinned( ctx, 2 * ( planned + 1 ) + 2 );
+		SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ctx->d_scalars + S_RR, sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+		SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + 1, ctx->d_scalars + S_BB, sizeof( double ), cudaMemcpyDeviceToHost,
+			st ) );
+		SLAB_CUDA( cudaStreamSynchronize( st ) );
+		const double b_norm = std::sqrt( ctx->h_pinned[ 1 ] );
+		const double denom = b_norm > 0.0 ? b_norm : 1.0;
+		double r_norm = std::sqrt( ctx->h_pinned[ 0 ] );
+		uint64_t count = 0;
+		history[ count++ ] = r_norm;
+
+		const bool already_converged = !fixed && r_norm / denom < cfg->rtol; // cg.hpp:103
+		const uint64_t limit = already_converged ? 0 : planned;
+
+		// iteration graph, cached per (x, config)
+		const bool graphs = ctx->use_graphs != 0;
+		if( graphs && limit > 0 ) {
+			if( !ctx->fused_transfers && cfg->use_preconditioner ) {
+				for( slab_level_s * at = H; at && at->R; at = at->coarser.get() ) {
+					mat_transposed( at->R.get() );
+				}
+			}
+			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
+				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
+				|| ws->key_fused != ctx->fused_transfers;
+			if( stale ) {
+				if( ws->iter_exec ) {
+					cudaGraphExecDestroy( ws->iter_exec );
+					ws->iter_exec = nullptr;
+				}
+				// reduction scratch must exist before capture (allocation is illegal while capturing)
+				ensure_partials( ctx, std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
+					kern::dot_tree_blocks( n, ctx->sm_count ) ) );
+				cudaGraph_t graph = nullptr;
+				const uint64_t before = g_launch_count;
+				SLAB_CUDA( cudaStreamBeginCapture( st, cudaStreamCaptureModeThreadLocal ) );
+				try {
+					iteration_enqueue( H, ws, x, cfg );
+				} catch( ... ) {
+					cudaStreamEndCapture( st, &graph );
+					if( graph ) {
+						cudaGraphDestroy( graph );
+					}
+					throw;
+				}
+				SLAB_CUDA( cudaStreamEndCapture( st, &graph ) );
+				ws->iter_launches = g_launch_count - before;
+				g_launch_count = before;
+				const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph, 0 );
+				cudaGraphDestroy( graph );
+				SLAB_CUDA( err );
+				ws->key_x = x->d;
+				ws->key_sweeps = cfg->sweeps;
+				ws->key_precond = cfg->use_preconditioner;
+				ws->key_dot = ctx->dot_mode;
+				ws->key_fused = ctx->fused_transfers;
+			}
+		}
+
+		const auto run_iteration = [ & ]() {
+			if( graphs ) {
+				SLAB_CUDA( cudaGraphLaunch( ws->iter_exec, st ) );
+				count_launch( ws->iter_launches );
+			} else {
+				iteration_enqueue( H, ws, x, cfg );
+			}
+			if( cfg->use_preconditioner ) {
+				vcycle_stats_all( H, cfg->sweeps );
+			}
+		};
+
+		int breakdown = 0;
+		if( fixed ) {
+			for( uint64_t iter = 1; iter <= limit; ++iter ) {
+				run_iteration();
+			}
+			if( limit > 0 ) {
+				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ws->d_hist_rr, limit * sizeof( double ), cudaMemcpyDeviceToHost,
+					st ) );
+				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + limit, ws->d_hist_pq, limit * sizeof( double ),
+					cudaMemcpyDeviceToHost, st ) );
+			}
+			SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
+			SLAB_CUDA( cudaStreamSynchronize( st ) );
+			for( uint64_t k = 0; k < limit; ++k ) {
+				if( ctx->h_pinned[ limit + k ] <= 0.0 ) { // cg.hpp:124-126
+					breakdown = 1;
+					break;
+				}
+				r_norm = std::sqrt( ctx->h_pinned[ k ] );
+				history[ count++ ] = r_norm;
+			}
+		} else {
+			for( uint64_t iter = 1; iter <= limit; ++iter ) {
+				run_iteration();
+				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ctx->d_scalars + S_RR, sizeof( double ), cudaMemcpyDeviceToHost,
+					st ) );
+				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + 1, ctx->d_scalars + S_PQ, sizeof( double ),
+					cudaMemcpyDeviceToHost, st ) );
+				SLAB_CUDA( cudaStreamSynchronize( st ) );
+				if( ctx->h_pinned[ 1 ] <= 0.0 ) {
+					breakdown = 1;
+					break;
+				}
+				r_norm = std::sqrt( ctx->h_pinned[ 0 ] );
+				history[ count++ ] = r_norm;
+				if( r_norm / denom < cfg->rtol ) { // cg.hpp:134-136
+					break;
+				}
+			}
+			SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
+			SLAB_CUDA( cudaStreamSynchronize( st ) );
+		}
+		float ms = 0.0f;
+		SLAB_CUDA( cudaEventElapsedTime( &ms, ctx->timer_start, ctx->timer_stop ) );
+		if( result ) {
+			result->iterations = count - 1;
+			result->converged = r_norm / denom < cfg->rtol ? 1 : 0;
+			result->solve_ms = ms;
+		}
+		if( breakdown ) {
+			fail( SLAB_ERR_SOLVER_BREAKDOWN, "cg_solve: p'Ap <= 0, operator is not SPD" );
+		}
+	}
+
+	// cg_solve with host buffers: the staging vectors live in the workspace so that the iteration
+	// graph (keyed by the solution vector) is captured once and replayed across calls.
+	void cg_solve_host( slab_level_s * H, const double * b, const double * x0, const slab_cg_config * cfg, double * x,
+		double * history, slab_cg_result * result ) {
+		slab_ctx_s * ctx = H->ctx;
+		const uint64_t n = H->n;
+		CgWorkspace * ws = workspace( H, 1 );
+		if( !ws->host_b ) {
+			ws->host_b.reset( vec_new( ctx, n, 0.0 ) );
+			ws->host_x.reset( vec_new( ctx, n, 0.0 ) );
+		}
+		if( n > 0 ) {
+			SLAB_CUDA( cudaMemcpyAsync( ws->host_b->d, b, n * sizeof( double ), cudaMemcpyHostToDevice, ctx->stream ) );
+			SLAB_CUDA( cudaMemcpyAsync( ws->host_x->d, x0, n * sizeof( double ), cudaMemcpyHostToDevice, ctx->stream ) );
+		}
+		cg_solve( H, ws->host_b.get(), ws->host_x.get(), cfg, ws->host_x.get(), history, result );
+		if( n > 0 ) {
+			SLAB_CUDA( cudaMemcpyAsync( x, ws->host_x->d, n * sizeof( double ), cudaMemcpyDeviceToHost, ctx->stream ) );
+			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+		}
+	}
+
+	// cg.hpp:59-67
+	double residual_norm( slab_mat_s * A, slab_vec_s * x, slab_vec_s * b ) {
+		if( A->nrows != b->n || A->ncols != x->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "residual_norm: operand sizes do not match the matrix" );
+		}
+		std::unique_ptr< slab_vec_s > r( vec_new( A->ctx, b->n, 0.0 ) );
+		op_mxv( r.get(), nullptr, A, x, SLAB_DESC_NONE );
+		op_waxpby( r.get(), 1.0, b, -1.0, r.get() );
+		const double rr = op_dot( r.get(), r.get() );
+		return std::sqrt( rr );
+	}
+
+} // namespace slabgpu

@@ -1,0 +1,218 @@
+// common.hpp — internal types shared by the translation units behind include/slab_b200.h.
+//
+// Data layout in HBM (DESIGN.md has the long version):
+//  * vectors: fp64, natural x-fastest order, n owned entries (+ ghost tail when decomposed);
+//  * matrices: SELL-32 — rows grouped in slices of 32, a slice stores its entries slot-major
+//    (slot k of all 32 rows contiguous: 256 B of values, 128 B of 32-bit column indices), slices
+//    have individual widths. Padding slots carry column -1 and are skipped, so a row sum runs
+//    over exactly the stored entries in ascending column order (operations.hpp:116-125);
+//  * a level keeps its matrix twice: rows in natural order (SpMV / residual) and rows grouped by
+//    colour (the Gauss-Seidel steps), each colour block padded to whole slices.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/slab_b200.h"
+
+namespace slabgpu {
+
+	struct Error {
+		int status;
+		std::string message;
+	};
+
+	[[noreturn]] inline void fail( int status, const std::string & message ) {
+		throw Error{ status, message };
+	}
+
+	inline void cuda_check( cudaError_t err, const char * what, const char * file, int line ) {
+		if( err != cudaSuccess ) {
+			fail( SLAB_ERR_CUDA, std::string( what ) + ": " + cudaGetErrorString( err ) + " (" + file + ":"
+				+ std::to_string( line ) + ")" );
+		}
+	}
+#define SLAB_CUDA( expr ) ::slabgpu::cuda_check( ( expr ), #expr, __FILE__, __LINE__ )
+
+	extern uint64_t g_launch_count;
+	inline void count_launch( uint64_t k = 1 ) {
+		g_launch_count += k;
+	}
+
+	constexpr int kSlice = 32;            // rows per SELL slice = one warp
+	constexpr uint64_t kDotChunk = 4096;  // parallel.hpp:70
+
+	// device scalar slots used by the CG driver (doubles in ctx->d_scalars)
+	enum Scalar { S_RHO = 0, S_RHO_PREV, S_PQ, S_RR, S_TMP, S_BB, S_COUNT = 16 };
+
+	struct Sell {
+		int64_t nrows = 0;     // logical rows (positions), multiple of kSlice not required
+		int64_t nslices = 0;
+		int64_t entries = 0;   // stored slots incl. padding
+		int64_t * slice_off = nullptr; // device, nslices+1, in entries
+		double * vals = nullptr;       // device
+		int32_t * cols = nullptr;      // device, -1 = padding
+		void release();
+		uint64_t bytes() const {
+			return static_cast< uint64_t >( entries ) * 12u + static_cast< uint64_t >( nslices + 1 ) * 8u;
+		}
+	};
+
+	struct CgWorkspace;
+
+} // namespace slabgpu
+
+struct slab_ctx_s {
+	int device = 0;
+	cudaStream_t stream = nullptr;
+	int sm_count = 0;
+	int cc_major = 0, cc_minor = 0;
+	uint64_t hbm_bytes = 0;
+	int dot_mode = SLAB_DOT_EXACT;
+	int use_graphs = 1;
+	int fused_transfers = 1;
+	double * d_scalars = nullptr;   // S_COUNT doubles
+	double * d_partials = nullptr;  // reduction scratch
+	uint64_t partials_cap = 0;
+	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
+	double * h_pinned = nullptr;    // pinned staging for scalar read-back
+	uint64_t h_pinned_cap = 0;
+	cudaEvent_t timer_start = nullptr, timer_stop = nullptr;
+};
+
+struct slab_vec_s {
+	slab_ctx_s * ctx = nullptr;
+	uint64_t n = 0;      // owned entries
+	uint64_t n_alloc = 0; // owned + ghost tail
+	double * d = nullptr;
+	~slab_vec_s() {
+		if( d ) {
+			cudaFree( d );
+		}
+	}
+};
+
+struct slab_mat_s {
+	slab_ctx_s * ctx = nullptr;
+	uint64_t nrows = 0, ncols = 0, nnz = 0;
+	slabgpu::Sell sell;             // natural row order
+	std::unique_ptr< slab_mat_s > transposed; // built lazily for SLAB_DESC_TRANSPOSE
+	// host CSR kept when the matrix came from slab_mat_create_csr (small, test-sized inputs)
+	std::vector< uint64_t > h_row_offsets, h_cols;
+	std::vector< double > h_vals;
+	bool has_host_csr = false;
+	~slab_mat_s() {
+		sell.release();
+	}
+};
+
+struct slab_mask_s {
+	slab_ctx_s * ctx = nullptr;
+	uint64_t universe = 0, count = 0;
+	int32_t * d_members = nullptr;
+	~slab_mask_s() {
+		if( d_members ) {
+			cudaFree( d_members );
+		}
+	}
+};
+
+struct slab_level_s {
+	slab_ctx_s * ctx = nullptr;
+	uint64_t dims[ 3 ] = { 0, 0, 0 };
+	uint64_t n = 0, nnz = 0;
+	bool is_stencil = false;
+	std::unique_ptr< slab_mat_s > A;       // natural-order SELL
+	slabgpu::Sell colorA;                  // colour-major SELL (positions)
+	int32_t * d_rows = nullptr;            // position -> natural row, -1 on padding
+	uint64_t num_colors = 0;
+	std::vector< int64_t > color_pos;      // first position of colour k (multiple of 32); size num_colors+1
+	std::vector< uint64_t > color_size;    // members per colour
+	std::vector< uint64_t > color_nnz;     // stored nonzeros per colour (problem.hpp:237-245)
+	std::unique_ptr< slab_vec_s > a_diag;
+	std::unique_ptr< slab_mat_s > R;       // restriction (n_c x n), null at the coarsest
+	std::unique_ptr< slab_level_s > coarser;
+	std::unique_ptr< slab_vec_s > s, f, r_c, z_c; // scratch (problem.hpp:228-231)
+	slab_level_stats stats{};
+	// V-cycle graph cache (keyed by the vectors it was captured with)
+	cudaGraphExec_t vcycle_exec = nullptr;
+	double * vcycle_z = nullptr;
+	double * vcycle_r = nullptr;
+	uint64_t vcycle_sweeps = 0;
+	int vcycle_fused = -1;
+	uint64_t vcycle_launches = 0;
+	// CG workspace of the hierarchy head: r, z, p, q, device history, iteration graph
+	std::unique_ptr< slabgpu::CgWorkspace > cg;
+	~slab_level_s();
+};
+
+namespace slabgpu {
+
+	struct CgWorkspace {
+		std::unique_ptr< slab_vec_s > r, z, p, q;
+		std::unique_ptr< slab_vec_s > host_b, host_x; // device staging of slab_cg_solve_host
+		double * d_hist_rr = nullptr;
+		double * d_hist_pq = nullptr;
+		unsigned int * d_iter = nullptr;
+		uint64_t hist_cap = 0;
+		cudaGraphExec_t iter_exec = nullptr;
+		double * key_x = nullptr;
+		uint64_t key_sweeps = 0;
+		int key_precond = -1, key_dot = -1, key_fused = -1;
+		uint64_t iter_launches = 0;
+		~CgWorkspace();
+	};
+
+	// ---- containers.cu
+	slab_vec_s * vec_new( slab_ctx_s * ctx, uint64_t n, double value );
+	void vec_free( slab_vec_s * v );
+	void ensure_partials( slab_ctx_s * ctx, uint64_t count );
+	void ensure_pinned( slab_ctx_s * ctx, uint64_t doubles );
+	double read_scalar( slab_ctx_s * ctx, int slot ); // syncs the stream
+	slab_mat_s * mat_from_csr( slab_ctx_s * ctx, uint64_t nrows, uint64_t ncols, const uint64_t * ro,
+		const uint64_t * co, const double * va, bool validate );
+	slab_mat_s * mat_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz );
+	slab_mat_s * mat_restriction( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz );
+	void mat_download_csr( slab_mat_s * A, uint64_t * ro, uint64_t * co, double * va );
+	slab_mat_s * mat_transposed( slab_mat_s * A );
+	// SELL over an arbitrary list of rows of a host CSR (row -1 = empty padding row)
+	Sell sell_from_csr_rows( slab_ctx_s * ctx, const std::vector< int64_t > & rows, const uint64_t * ro,
+		const uint64_t * co, const double * va );
+	// SELL of the 27-point stencil over an arbitrary device row list (d_rows == nullptr: natural order)
+	Sell sell_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, const int32_t * d_rows,
+		int64_t npos );
+
+	// ---- level.cu
+	slab_level_s * hierarchy_create( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t levels );
+	slab_level_s * level_from_csr( slab_ctx_s * ctx, uint64_t n, const uint64_t * ro, const uint64_t * co,
+		const double * va );
+	void rbgs_color_step( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r );
+	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r );
+	void rbgs_backward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r );
+	void rbgs_symmetric( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
+	void restrict_vector( slab_level_s * L, slab_vec_s * v_fine, slab_vec_s * out );
+	void refine_and_add( slab_level_s * L, slab_vec_s * z, slab_vec_s * z_c );
+	void mg_vcycle( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats );
+
+	// ---- ops (kernels.cu)
+	void op_set_all( slab_vec_s * v, double value );
+	void op_waxpby( slab_vec_s * w, double alpha, slab_vec_s * x, double beta, slab_vec_s * y );
+	void op_dot_to_slot( slab_vec_s * x, slab_vec_s * y, int slot ); // result -> ctx->d_scalars[slot]
+	double op_dot( slab_vec_s * x, slab_vec_s * y );
+	void op_mxv( slab_vec_s * y, slab_mask_s * mask, slab_mat_s * A, slab_vec_s * x, unsigned desc );
+
+	// ---- cg.cu
+	void cg_solve( slab_level_s * H, slab_vec_s * b, slab_vec_s * x0, const slab_cg_config * cfg, slab_vec_s * x,
+		double * history, slab_cg_result * result );
+	void cg_solve_host( slab_level_s * H, const double * b, const double * x0, const slab_cg_config * cfg, double * x,
+		double * history, slab_cg_result * result );
+	double residual_norm( slab_mat_s * A, slab_vec_s * x, slab_vec_s * b );
+
+} // namespace slabgpu

@@ -1,0 +1,72 @@
+// kernels.cuh — launch wrappers of the hand-written sm_100a kernels (kernels.cu).
+// Every wrapper enqueues on the given stream and returns immediately.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace slabgpu {
+	namespace kern {
+
+		// ---- vector ops (operations.hpp:49-106)
+		void fill( cudaStream_t st, double * v, uint64_t n, double value );
+		void waxpby( cudaStream_t st, double * w, double alpha, const double * x, double beta, const double * y,
+			uint64_t n );
+		// dot, exact: 4096-chunk ordered (operations.hpp:61-91). partials needs ceil(n/4096) doubles.
+		void dot_exact( cudaStream_t st, const double * x, const double * y, uint64_t n, double * partials,
+			unsigned int * counter, double * out );
+		// dot, fixed-shape tree. partials needs dot_tree_blocks(n, sms) doubles.
+		uint64_t dot_tree_blocks( uint64_t n, int sm_count );
+		void dot_tree( cudaStream_t st, const double * x, const double * y, uint64_t n, int sm_count, double * partials,
+			unsigned int * counter, double * out );
+
+		// ---- SELL-32 matrix-vector products (operations.hpp:116-125, :164-174)
+		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
+			const double * x, double * y, int64_t nrows );
+		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
+			const double * x, double * y, const int32_t * members, int64_t count );
+
+		// ---- fused Gauss-Seidel colour step (smoother.hpp:60-72) on the colour-major SELL
+		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
+			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r );
+
+		// ---- fused grid transfers (multigrid.hpp:100-104 and :71-81)
+		// r_c[p] = 0 + 1*( 1*r[i] + (-1)*(A z)[i] ),  i = rows[p], p in the colour-0 block = injected rows
+		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
+			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c );
+		// z[i] = 1*z[i] + 1*(0 + 1*z_c[p]) at the injected rows
+		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c );
+
+		// ---- CG vector updates with device-resident scalars (cg.hpp:116-132)
+		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)
+		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,
+			const unsigned int * iter_counter, uint64_t n );
+		// alpha = rho/pq; x = 1*x + alpha*p; r = 1*r + (-alpha)*q; rho_prev <- rho
+		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
+			uint64_t n );
+		// hist_rr[it] = rr, hist_pq[it] = pq, ++it
+		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,
+			unsigned int * iter_counter );
+
+		// ---- setup: 27-point stencil straight into SELL (problem.hpp:90-131), colour row lists
+		void stencil_widths( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos,
+			int64_t nslices, int32_t * widths );
+		void stencil_fill( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
+			const int64_t * slice_off, double * vals, int32_t * cols );
+		// rows[pos0 + q] = natural index of the q-th member of parity class (px,py,pz), -1 beyond `size`
+		void color_rows( cudaStream_t st, int nx, int ny, int nz, int px, int py, int pz, int64_t pos0, int64_t size,
+			int64_t padded, int32_t * rows );
+		// fine[c] = linear index of (2cx,2cy,2cz) (problem.hpp:189-195)
+		void injection_cols( cudaStream_t st, int nx, int ny, int nz, int32_t * fine );
+		// widths/cols/vals of a one-entry-per-row SELL from a column list
+		void sell_single_entry( cudaStream_t st, const int32_t * col_of_row, int64_t nrows, int64_t nslices,
+			double * vals, int32_t * cols );
+		// SELL -> row counts / CSR (download path)
+		void sell_row_counts( cudaStream_t st, const int64_t * slice_off, const int32_t * cols, int64_t nrows,
+			int64_t * counts );
+		void sell_to_csr( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
+			int64_t nrows, const int64_t * row_off, int64_t * out_cols, double * out_vals );
+
+	} // namespace kern
+} // namespace slabgpu

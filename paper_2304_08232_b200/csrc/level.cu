@@ -1,0 +1,413 @@
+// level.cu — multigrid levels (problem.hpp:220-319), the coloured Gauss-Seidel smoother
+// (smoother.hpp) and the V-cycle (multigrid.hpp) on top of the kernels.
+#include <algorithm>
+#include <limits>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+slab_level_s::~slab_level_s() {
+	colorA.release();
+	if( d_rows ) {
+		cudaFree( d_rows );
+	}
+	if( vcycle_exec ) {
+		cudaGraphExecDestroy( vcycle_exec );
+	}
+}
+
+namespace slabgpu {
+
+	namespace {
+
+		int64_t round_up( int64_t v, int64_t m ) {
+			return ( v + m - 1 ) / m * m;
+		}
+
+		// sum over the points of one parity class along one axis of the 1D neighbour count
+		uint64_t span_sum( uint64_t n, uint64_t parity ) {
+			uint64_t total = 0;
+			for( uint64_t i = parity; i < n; i += 2 ) {
+				total += ( i > 0 ? 1 : 0 ) + 1 + ( i + 1 < n ? 1 : 0 );
+			}
+			return total;
+		}
+
+		void alloc_scratch( slab_level_s * L, uint64_t n_coarse ) {
+			L->f.reset( vec_new( L->ctx, L->n, 0.0 ) );
+			if( n_coarse > 0 ) {
+				L->r_c.reset( vec_new( L->ctx, n_coarse, 0.0 ) );
+				L->z_c.reset( vec_new( L->ctx, n_coarse, 0.0 ) );
+			}
+		}
+
+		// One stencil level, generated on the device. The colouring is the closed form of what
+		// greedy_color (coloring.hpp:114-158) finds on every 27-point grid: colour k is the parity
+		// class ix%2 + 2*(iy%2) + 4*(iz%2), members ascending (tests pin this against the oracle's
+		// greedy colouring, even and odd dimensions).
+		slab_level_s * stencil_level( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, bool with_restriction ) {
+			std::unique_ptr< slab_level_s > L( new slab_level_s );
+			L->ctx = ctx;
+			L->dims[ 0 ] = nx;
+			L->dims[ 1 ] = ny;
+			L->dims[ 2 ] = nz;
+			L->is_stencil = true;
+			L->A.reset( mat_stencil27( ctx, nx, ny, nz ) );
+			L->n = L->A->nrows;
+			L->nnz = L->A->nnz;
+			L->num_colors = 8;
+			L->color_pos.assign( 9, 0 );
+			L->color_size.assign( 8, 0 );
+			L->color_nnz.assign( 8, 0 );
+			for( int k = 0; k < 8; ++k ) {
+				const uint64_t px = k & 1, py = ( k >> 1 ) & 1, pz = ( k >> 2 ) & 1;
+				const uint64_t sx = ( nx + 1 - px ) / 2, sy = ( ny + 1 - py ) / 2, sz = ( nz + 1 - pz ) / 2;
+				L->color_size[ k ] = sx * sy * sz;
+				L->color_nnz[ k ] = span_sum( nx, px ) * span_sum( ny, py ) * span_sum( nz, pz );
+				L->color_pos[ k + 1 ] = L->color_pos[ k ] + round_up( static_cast< int64_t >( L->color_size[ k ] ), kSlice );
+			}
+			const int64_t npos = L->color_pos[ 8 ];
+			SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< int64_t >( npos, 1 ) * sizeof( int32_t ) ) );
+			for( int k = 0; k < 8; ++k ) {
+				kern::color_rows( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
+					k & 1, ( k >> 1 ) & 1, ( k >> 2 ) & 1, L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ),
+					L->color_pos[ k + 1 ] - L->color_pos[ k ], L->d_rows );
+			}
+			L->colorA = sell_stencil27( ctx, nx, ny, nz, L->d_rows, npos );
+			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
+			uint64_t n_coarse = 0;
+			if( with_restriction ) {
+				L->R.reset( mat_restriction( ctx, nx, ny, nz ) );
+				n_coarse = L->R->nrows;
+			}
+			alloc_scratch( L.get(), n_coarse );
+			return L.release();
+		}
+
+	} // namespace
+
+	// problem.hpp:284-319
+	slab_level_s * hierarchy_create( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t levels ) {
+		if( nx < 2 || ny < 2 || nz < 2 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "grid dimensions must all be at least 2, got " + std::to_string( nx ) + "x"
+				+ std::to_string( ny ) + "x" + std::to_string( nz ) );
+		}
+		if( levels < 1 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "build_hierarchy: need at least one level" );
+		}
+		if( levels > 40 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "build_hierarchy: too many levels" );
+		}
+		const uint64_t divider = uint64_t( 1 ) << ( levels - 1 );
+		const uint64_t d[ 3 ] = { nx, ny, nz };
+		const char * names[ 3 ] = { "nx", "ny", "nz" };
+		for( int a = 0; a < 3; ++a ) {
+			if( d[ a ] % divider != 0 ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, std::string( "build_hierarchy: dimension " ) + names[ a ] + " = "
+					+ std::to_string( d[ a ] ) + " is not divisible by 2^(levels-1) = " + std::to_string( divider ) );
+			}
+			if( d[ a ] / divider < 2 ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, std::string( "build_hierarchy: dimension " ) + names[ a ] + " = "
+					+ std::to_string( d[ a ] ) + " becomes smaller than 2 after " + std::to_string( levels - 1 ) + " halvings" );
+			}
+		}
+		std::unique_ptr< slab_level_s > head;
+		slab_level_s * tail = nullptr;
+		uint64_t lx = nx, ly = ny, lz = nz;
+		for( uint64_t k = 0; k < levels; ++k ) {
+			std::unique_ptr< slab_level_s > L( stencil_level( ctx, lx, ly, lz, k + 1 < levels ) );
+			slab_level_s * raw = L.get();
+			if( tail == nullptr ) {
+				head = std::move( L );
+			} else {
+				tail->coarser = std::move( L );
+			}
+			tail = raw;
+			lx /= 2;
+			ly /= 2;
+			lz /= 2;
+		}
+		return head.release();
+	}
+
+	// ProblemLevel(SparseMatrix) problem.hpp:253 for an arbitrary square system. Setup runs on the
+	// host exactly like the reference's: extract_diagonal (problem.hpp:143-166) and greedy_color
+	// (coloring.hpp:114-158) over pattern(A) united with pattern(A^T), rows in increasing order,
+	// smallest colour not used by an already coloured neighbour.
+	slab_level_s * level_from_csr( slab_ctx_s * ctx, uint64_t n, const uint64_t * ro, const uint64_t * co,
+		const double * va ) {
+		std::unique_ptr< slab_level_s > L( new slab_level_s );
+		L->ctx = ctx;
+		L->dims[ 0 ] = n;
+		L->dims[ 1 ] = 1;
+		L->dims[ 2 ] = 1;
+		L->A.reset( mat_from_csr( ctx, n, n, ro, co, va, true ) );
+		L->n = n;
+		L->nnz = L->A->nnz;
+
+		std::vector< double > diag( n );
+		for( uint64_t i = 0; i < n; ++i ) {
+			const uint64_t * first = co + ro[ i ];
+			const uint64_t * last = co + ro[ i + 1 ];
+			const uint64_t * hit = std::lower_bound( first, last, i );
+			if( hit == last || *hit != i || va[ hit - co ] == 0.0 ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, "extract_diagonal: row " + std::to_string( i ) + " has no usable diagonal entry" );
+			}
+			diag[ i ] = va[ hit - co ];
+		}
+
+		// adjacency of the transpose pattern, so that non-symmetric patterns colour like the reference
+		std::vector< uint64_t > t_off( n + 1, 0 );
+		for( uint64_t k = 0; k < L->nnz; ++k ) {
+			++t_off[ co[ k ] + 1 ];
+		}
+		for( uint64_t i = 0; i < n; ++i ) {
+			t_off[ i + 1 ] += t_off[ i ];
+		}
+		std::vector< uint64_t > t_idx( L->nnz ), cursor( t_off.begin(), t_off.end() - 1 );
+		for( uint64_t i = 0; i < n; ++i ) {
+			for( uint64_t k = ro[ i ]; k < ro[ i + 1 ]; ++k ) {
+				t_idx[ cursor[ co[ k ] ]++ ] = i;
+			}
+		}
+		constexpr uint64_t unset = std::numeric_limits< uint64_t >::max();
+		std::vector< uint64_t > color( n, unset );
+		std::vector< uint64_t > stamp; // stamp[c] == i  <=>  colour c is taken around row i
+		uint64_t num_colors = 0;
+		for( uint64_t i = 0; i < n; ++i ) {
+			const auto forbid = [ & ]( uint64_t j ) {
+				if( j != i && color[ j ] != unset ) {
+					if( color[ j ] >= stamp.size() ) {
+						stamp.resize( color[ j ] + 1, unset );
+					}
+					stamp[ color[ j ] ] = i;
+				}
+			};
+			for( uint64_t k = ro[ i ]; k < ro[ i + 1 ]; ++k ) {
+				forbid( co[ k ] );
+			}
+			for( uint64_t k = t_off[ i ]; k < t_off[ i + 1 ]; ++k ) {
+				forbid( t_idx[ k ] );
+			}
+			uint64_t pick = 0;
+			while( pick < stamp.size() && stamp[ pick ] == i ) {
+				++pick;
+			}
+			color[ i ] = pick;
+			num_colors = std::max( num_colors, pick + 1 );
+		}
+
+		L->num_colors = num_colors;
+		L->color_size.assign( num_colors, 0 );
+		L->color_nnz.assign( num_colors, 0 );
+		for( uint64_t i = 0; i < n; ++i ) {
+			++L->color_size[ color[ i ] ];
+			L->color_nnz[ color[ i ] ] += ro[ i + 1 ] - ro[ i ];
+		}
+		L->color_pos.assign( num_colors + 1, 0 );
+		for( uint64_t k = 0; k < num_colors; ++k ) {
+			L->color_pos[ k + 1 ] = L->color_pos[ k ] + round_up( static_cast< int64_t >( L->color_size[ k ] ), kSlice );
+		}
+		std::vector< int64_t > rows( L->color_pos[ num_colors ], -1 );
+		std::vector< int64_t > fill( L->color_pos.begin(), L->color_pos.end() - 1 );
+		for( uint64_t i = 0; i < n; ++i ) {
+			rows[ fill[ color[ i ] ]++ ] = static_cast< int64_t >( i ); // ascending i keeps members sorted
+		}
+		L->colorA = sell_from_csr_rows( ctx, rows, ro, co, va );
+		std::vector< int32_t > rows32( rows.begin(), rows.end() );
+		SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< size_t >( rows32.size(), 1 ) * sizeof( int32_t ) ) );
+		SLAB_CUDA( cudaMemcpy( L->d_rows, rows32.data(), rows32.size() * sizeof( int32_t ), cudaMemcpyHostToDevice ) );
+		L->a_diag.reset( vec_new( ctx, n, 0.0 ) );
+		SLAB_CUDA( cudaMemcpy( L->a_diag->d, diag.data(), n * sizeof( double ), cudaMemcpyHostToDevice ) );
+		alloc_scratch( L.get(), 0 );
+		return L.release();
+	}
+
+	// ---------------------------------------------------------------- smoother.hpp
+
+	namespace {
+		void check_smoother_args( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:54-58
+			if( z->n != L->n || r->n != L->n ) {
+				fail( SLAB_ERR_DIMENSION_MISMATCH, "smoother: vector lengths differ from the level size" );
+			}
+		}
+
+		void color_step_enqueue( slab_level_s * L, uint64_t k, double * z, const double * r ) {
+			kern::gs_color_step( L->ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z, r );
+		}
+
+		void forward_enqueue( slab_level_s * L, double * z, const double * r ) { // smoother.hpp:80-82
+			for( uint64_t k = 0; k < L->num_colors; ++k ) {
+				color_step_enqueue( L, k, z, r );
+			}
+		}
+
+		void backward_enqueue( slab_level_s * L, double * z, const double * r ) { // smoother.hpp:95-97
+			for( uint64_t k = L->num_colors; k > 0; --k ) {
+				color_step_enqueue( L, k - 1, z, r );
+			}
+		}
+
+		void symmetric_enqueue( slab_level_s * L, double * z, const double * r, uint64_t sweeps ) { // smoother.hpp:108-111
+			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
+				forward_enqueue( L, z, r );
+				backward_enqueue( L, z, r );
+			}
+		}
+	} // namespace
+
+	void rbgs_color_step( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r ) {
+		check_smoother_args( L, z, r );
+		if( k >= L->num_colors ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "rbgs_color_step: colour index out of range" );
+		}
+		color_step_enqueue( L, k, z->d, r->d );
+		L->stats.nnz_visited += L->color_nnz[ k ]; // smoother.hpp:71
+	}
+
+	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
+		check_smoother_args( L, z, r );
+		forward_enqueue( L, z->d, r->d );
+		L->stats.nnz_visited += L->nnz;
+	}
+
+	void rbgs_backward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
+		check_smoother_args( L, z, r );
+		backward_enqueue( L, z->d, r->d );
+		L->stats.nnz_visited += L->nnz;
+	}
+
+	void rbgs_symmetric( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
+		if( sweeps < 1 ) { // smoother.hpp:105-107
+			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
+		}
+		check_smoother_args( L, z, r );
+		symmetric_enqueue( L, z->d, r->d, sweeps );
+		L->stats.nnz_visited += 2 * sweeps * L->nnz;
+	}
+
+	// ---------------------------------------------------------------- multigrid.hpp
+
+	void restrict_vector( slab_level_s * L, slab_vec_s * v_fine, slab_vec_s * out ) { // multigrid.hpp:46-54
+		if( !L->R ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "restrict_vector: the coarsest level has no restriction operator" );
+		}
+		op_mxv( out, nullptr, L->R.get(), v_fine, SLAB_DESC_NONE );
+		L->stats.nnz_visited += L->R->nnz;
+	}
+
+	void refine_and_add( slab_level_s * L, slab_vec_s * z, slab_vec_s * z_c ) { // multigrid.hpp:71-81
+		if( !L->R ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "refine_and_add: the coarsest level has no restriction operator" );
+		}
+		if( z_c->n != L->R->nrows || z->n != L->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "mxv: operand sizes do not match the matrix" );
+		}
+		if( L->ctx->fused_transfers ) {
+			// injected rows are the colour-0 block: position p <-> coarse index p
+			kern::prolong_add( L->ctx->stream, L->d_rows, static_cast< int64_t >( z_c->n ), z->d, z_c->d );
+		} else {
+			op_mxv( L->f.get(), nullptr, L->R.get(), z_c, SLAB_DESC_TRANSPOSE );
+			op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+		}
+		L->stats.nnz_visited += L->R->nnz;
+	}
+
+	namespace {
+		void vcycle_stats( slab_level_s * L, uint64_t sweeps ) {
+			if( !L->coarser ) {
+				L->stats.nnz_visited += 2 * sweeps * L->nnz;
+				return;
+			}
+			// two symmetric smooths, the residual pass, restriction and refinement
+			L->stats.nnz_visited += 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz;
+			vcycle_stats( L->coarser.get(), sweeps );
+		}
+	} // namespace
+
+	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats ) {
+		slab_ctx_s * ctx = L->ctx;
+		symmetric_enqueue( L, z->d, r->d, sweeps );
+		if( !L->coarser ) {
+			if( count_stats ) {
+				L->stats.nnz_visited += 2 * sweeps * L->nnz;
+			}
+			return;
+		}
+		if( ctx->fused_transfers ) {
+			kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d );
+		} else {
+			op_mxv( L->f.get(), nullptr, L->A.get(), z, SLAB_DESC_NONE ); // f <- A z
+			op_waxpby( L->f.get(), 1.0, r, -1.0, L->f.get() );            // f <- r - f
+			op_mxv( L->r_c.get(), nullptr, L->R.get(), L->f.get(), SLAB_DESC_NONE );
+		}
+		op_set_all( L->z_c.get(), 0.0 );
+		mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
+		if( ctx->fused_transfers ) {
+			kern::prolong_add( ctx->stream, L->d_rows, static_cast< int64_t >( L->z_c->n ), z->d, L->z_c->d );
+		} else {
+			op_mxv( L->f.get(), nullptr, L->R.get(), L->z_c.get(), SLAB_DESC_TRANSPOSE );
+			op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+		}
+		symmetric_enqueue( L, z->d, r->d, sweeps );
+		if( count_stats ) {
+			L->stats.nnz_visited += 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz;
+		}
+	}
+
+	void mg_vcycle( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
+		if( z->n != L->n || r->n != L->n ) { // multigrid.hpp:89-91
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "mg_vcycle: vector lengths differ from the level size" );
+		}
+		if( sweeps < 1 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
+		}
+		slab_ctx_s * ctx = L->ctx;
+		if( !ctx->use_graphs ) {
+			mg_vcycle_enqueue( L, z, r, sweeps, true );
+			return;
+		}
+		// make sure lazily built transposes exist before capturing (they allocate)
+		if( !ctx->fused_transfers ) {
+			for( slab_level_s * at = L; at && at->R; at = at->coarser.get() ) {
+				mat_transposed( at->R.get() );
+			}
+		}
+		if( L->vcycle_exec == nullptr || L->vcycle_z != z->d || L->vcycle_r != r->d || L->vcycle_sweeps != sweeps
+			|| L->vcycle_fused != ctx->fused_transfers ) {
+			if( L->vcycle_exec ) {
+				cudaGraphExecDestroy( L->vcycle_exec );
+				L->vcycle_exec = nullptr;
+			}
+			cudaGraph_t graph = nullptr;
+			const uint64_t launches_before = g_launch_count;
+			SLAB_CUDA( cudaStreamBeginCapture( ctx->stream, cudaStreamCaptureModeThreadLocal ) );
+			try {
+				mg_vcycle_enqueue( L, z, r, sweeps, false );
+			} catch( ... ) {
+				cudaStreamEndCapture( ctx->stream, &graph );
+				if( graph ) {
+					cudaGraphDestroy( graph );
+				}
+				throw;
+			}
+			SLAB_CUDA( cudaStreamEndCapture( ctx->stream, &graph ) );
+			L->vcycle_launches = g_launch_count - launches_before;
+			g_launch_count = launches_before;
+			const cudaError_t err = cudaGraphInstantiate( &L->vcycle_exec, graph, 0 );
+			cudaGraphDestroy( graph );
+			SLAB_CUDA( err );
+			L->vcycle_z = z->d;
+			L->vcycle_r = r->d;
+			L->vcycle_sweeps = sweeps;
+			L->vcycle_fused = ctx->fused_transfers;
+		}
+		SLAB_CUDA( cudaGraphLaunch( L->vcycle_exec, ctx->stream ) );
+		count_launch( L->vcycle_launches );
+		vcycle_stats( L, sweeps );
+	}
+
+} // namespace slabgpu

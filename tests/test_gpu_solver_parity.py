@@ -1,0 +1,146 @@
+"""GPU parity of the CG+MG hot path against the CPU oracle (bit-exact) and the committed golden
+residual histories generated from the reference headers (tests/golden/make_golden.py).
+
+Everything goes through the C ABI (include/slab_b200.h) via the reference-shaped mirror in
+paper_2304_08232_b200. Tolerances: SpMV, the colour steps, transfers, waxpby and the exact dot
+are compared bitwise; BASELINE.json's bar for residual histories is 1e-10 relative per
+iteration, the tests below demand equality in exact-dot mode and 1e-10 in tree-dot mode.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as fh:
+        return json.load(fh)
+
+
+def _rhs_A_ones(slab, ctx, h):
+    ones = ctx.DenseVector(h.n(), 1.0)
+    b = ctx.DenseVector(h.n())
+    slab.mxv(b, h.A, ones)  # b = A*1 with the library's own SpMV
+    return b
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_residual_history_matches_reference_golden(slab, ctx, n):
+    """BASELINE.json configs[0] and configs[1]: 4 levels, 50 fixed iterations, b = A*1, x0 = 0."""
+    gold = _golden(f"history_{n}.json")
+    ctx.dot_mode = slab.DOT_EXACT
+    h = ctx.build_hierarchy((n, n, n), 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=50, fixed_iterations=50))
+    assert res.iterations == gold["iterations"] == 50
+    got = np.array(res.residual_history)
+    want = np.array(gold["residual_history"])
+    assert got.shape == want.shape
+    # exact-dot mode reproduces the reference's arithmetic order: identical doubles
+    assert np.array_equal(got, want), f"max rel diff {np.max(np.abs(got - want) / want)}"
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_solution_and_history_match_oracle_bitwise(slab, ctx, oracle, n):
+    ctx.dot_mode = slab.DOT_EXACT
+    h = ctx.build_hierarchy((n, n, n), 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=20, fixed_iterations=20))
+    oh = oracle.build_hierarchy(n, n, n, 4)
+    ob = oracle.level_mxv(oh, np.ones(oh.n))
+    assert np.array_equal(b.values(), ob)
+    ores = oracle.cg_solve(oh, ob, np.zeros(oh.n), max_iters=20, fixed_iterations=20)
+    assert res.residual_history == ores.residual_history
+    assert np.array_equal(res.solution.values(), ores.solution)
+
+
+def test_tree_dot_history_within_1e10_at_64(slab, ctx):
+    """The fast (tree) dot re-associates the reductions; at 64^3 the reference history must still be
+    matched to BASELINE.json's 1e-10 relative tolerance per iteration."""
+    gold = _golden("history_64.json")
+    ctx.dot_mode = slab.DOT_TREE
+    try:
+        h = ctx.build_hierarchy((64, 64, 64), 4)
+        b = _rhs_A_ones(slab, ctx, h)
+        res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=50, fixed_iterations=50))
+    finally:
+        ctx.dot_mode = slab.DOT_EXACT
+    got = np.array(res.residual_history)
+    want = np.array(gold["residual_history"])
+    rel = np.abs(got - want) / want
+    assert res.iterations == 50
+    assert rel.max() <= 1e-10, rel.max()
+
+
+def test_graphs_and_eager_agree_bitwise(slab, ctx):
+    h = ctx.build_hierarchy((16, 16, 16), 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    cfg = slab.CGConfig(max_iters=12, fixed_iterations=12)
+    with_graphs = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), cfg)
+    ctx.set_graphs(False)
+    try:
+        eager = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), cfg)
+    finally:
+        ctx.set_graphs(True)
+    assert with_graphs.residual_history == eager.residual_history
+    assert with_graphs.solution == eager.solution
+
+
+def test_fused_and_unfused_transfers_agree(slab, ctx):
+    """The fused residual+restriction / prolongation kernels against the reference's
+    primitive-by-primitive composition (multigrid.hpp:100-104, :76-77), same device."""
+    h = ctx.build_hierarchy((16, 16, 16), 3)
+    r, _ = ctx.random_vector(h.n(), 5)
+    z_fused = ctx.DenseVector(h.n(), 0.0)
+    slab.mg_vcycle(h, z_fused, r)
+    ctx.set_fused_transfers(False)
+    try:
+        z_plain = ctx.DenseVector(h.n(), 0.0)
+        slab.mg_vcycle(h, z_plain, r)
+    finally:
+        ctx.set_fused_transfers(True)
+    assert z_fused == z_plain
+
+
+def test_convergence_mode_matches_oracle(slab, ctx, oracle):
+    """rtol-driven exit (cg.hpp:134-136): same iteration count, history and flag as the oracle."""
+    n = 16
+    h = ctx.build_hierarchy((n, n, n), 4)
+    b = ctx.build_rhs((n, n, n))
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(rtol=1e-9))
+    oh = oracle.build_hierarchy(n, n, n, 4)
+    ores = oracle.cg_solve(oh, np.ones(oh.n), np.zeros(oh.n), rtol=1e-9)
+    assert res.iterations == ores.iterations
+    assert res.converged and ores.converged
+    assert res.residual_history == ores.residual_history
+    assert np.array_equal(res.solution.values(), ores.solution)
+
+
+def test_host_buffer_entry_point_matches_device_entry_point(slab, ctx):
+    n = 16
+    h = ctx.build_hierarchy((n, n, n), 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    cfg = slab.CGConfig(max_iters=10, fixed_iterations=10)
+    dev = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), cfg)
+    host = slab.cg_solve_host(h, b.values(), np.zeros(h.n()), cfg)
+    assert dev.residual_history == host.residual_history
+    assert np.array_equal(dev.solution.values(), host.solution)
+
+
+def test_odd_coarse_grid_hierarchy_matches_oracle(slab, ctx, oracle):
+    """104^3-shaped chain in miniature: 24 -> 12 -> 6 -> 3 puts an odd grid at the coarsest level,
+    where the parity classes have unequal sizes (the 104 -> 13 case of BASELINE configs[3])."""
+    dims = (24, 24, 24)
+    h = ctx.build_hierarchy(dims, 4)
+    oh = oracle.build_hierarchy(*dims, 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    ob = oracle.level_mxv(oh, np.ones(oh.n))
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=15, fixed_iterations=15))
+    ores = oracle.cg_solve(oh, ob, np.zeros(oh.n), max_iters=15, fixed_iterations=15)
+    assert res.residual_history == ores.residual_history
+    assert np.array_equal(res.solution.values(), ores.solution)
