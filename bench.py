@@ -278,12 +278,21 @@ def measured_traffic(dims):
         return None
 
 
-def time_solves(slab, ctx, h, b, x0, cfg, count):
+def time_solves(slab, ctx, h, b, x0, cfg, count, x):
+    """CUDA events on the library's stream around `count` solves; cross-checked against the host
+    clock (every solve ends with a stream synchronisation, so the two must agree)."""
+    ctx.sync()
+    t0 = time.perf_counter()
     ctx.timer_start()
     res = None
+    inner = 0.0
     for _ in range(count):
-        res = slab.cg_solve(h, b, x0, cfg)
+        res = slab.cg_solve(h, b, x0, cfg, out=x)
+        inner += res.solve_ms
     ms = ctx.timer_stop()
+    wall = (time.perf_counter() - t0) * 1e3
+    if count and not (inner <= ms * 1.001 + 0.05 and ms <= wall * 1.001 + 0.05):
+        raise RuntimeError(f"inconsistent clocks: solves {inner:.3f} ms, events {ms:.3f} ms, host {wall:.3f} ms")
     return ms, res
 
 
@@ -296,9 +305,10 @@ def bench_one(slab, ctx, dims, steps, warmup, dot_mode):
     slab.mxv(b, h.A, ones)
     x0 = ctx.DenseVector(n, 0.0)
     cfg = slab.CGConfig(max_iters=CG_ITERS, fixed_iterations=CG_ITERS)
-    time_solves(slab, ctx, h, b, x0, cfg, warmup)
+    x = ctx.DenseVector(n)
+    time_solves(slab, ctx, h, b, x0, cfg, warmup, x)
     launches0 = slab.launch_count()
-    ms, res = time_solves(slab, ctx, h, b, x0, cfg, steps)
+    ms, res = time_solves(slab, ctx, h, b, x0, cfg, steps, x)
     launches = slab.launch_count() - launches0
     flops = hpcg_flops_per_iteration(dims) * CG_ITERS * steps
     return {"h": h, "b": b, "x0": x0, "cfg": cfg, "ms": ms, "res": res, "launches": launches,

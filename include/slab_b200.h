@@ -66,6 +66,8 @@ const char * slab_last_error( void );
 const char * slab_status_name( int status );
 /* number of kernels this library has launched in this process (bench.py's gpu_launches) */
 uint64_t slab_launch_count( void );
+/* chain kernels with programmatic dependent launch (griddepcontrol): 1 (default) or 0. Process-wide. */
+int slab_set_programmatic_launch( int enabled );
 
 /* ------------------------------------------------------------------ context */
 int slab_ctx_create( int device, slab_ctx_t * out );

@@ -97,6 +97,7 @@ SIGNATURES = {
     "slab_last_error": (C.c_char_p, []),
     "slab_status_name": (C.c_char_p, [C.c_int]),
     "slab_launch_count": (_u64, []),
+    "slab_set_programmatic_launch": (C.c_int, [C.c_int]),
     "slab_ctx_create": (C.c_int, [C.c_int, _pvp]),
     "slab_ctx_destroy": (C.c_int, [_vp]),
     "slab_ctx_sync": (C.c_int, [_vp]),
@@ -178,6 +179,10 @@ def _check(rc: int) -> None:
     if rc != 0:
         msg = _lib.slab_last_error().decode(errors="replace")
         raise _STATUS.get(rc, Error)(msg)
+
+
+def set_programmatic_launch(enabled: bool) -> None:
+    _check(load_library().slab_set_programmatic_launch(int(enabled)))
 
 
 def launch_count() -> int:
@@ -667,11 +672,13 @@ def _history_len(cfg: CGConfig) -> int:
 
 
 def cg_solve(hierarchy: ProblemLevel, b: DenseVector, x0: DenseVector, cfg: CGConfig = CGConfig(),
-             smoother_cfg: SmootherConfig = SmootherConfig()) -> CGResult:
+             smoother_cfg: SmootherConfig = SmootherConfig(), out: Optional[DenseVector] = None) -> CGResult:
+    """cg.hpp:77-142. `out` optionally supplies the solution vector (the reference returns a fresh
+    one); reusing it across calls lets the library replay its cached iteration graph."""
     cc = _c_config(cfg, smoother_cfg)
     hist = np.zeros(_history_len(cfg), dtype=np.float64)
     res = _CgResult()
-    x = DenseVector(hierarchy.ctx, hierarchy.n())
+    x = out if out is not None else DenseVector(hierarchy.ctx, hierarchy.n())
     _check(_lib.slab_cg_solve(hierarchy._h, b._h, x0._h, C.byref(cc), x._h, _ptr(hist), C.byref(res)))
     k = int(res.iterations)
     return CGResult(k, [float(v) for v in hist[: k + 1]], bool(res.converged), x, float(res.solve_ms))

@@ -68,6 +68,11 @@ const char * slab_status_name( int status ) {
 	}
 }
 
+int slab_set_programmatic_launch( int enabled ) {
+	g_use_pdl = enabled ? 1 : 0;
+	return SLAB_OK;
+}
+
 uint64_t slab_launch_count( void ) {
 	return g_launch_count;
 }
@@ -105,8 +110,11 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		SLAB_CUDA( cudaMemset( ctx->d_scalars, 0, S_COUNT * sizeof( double ) ) );
 		SLAB_CUDA( cudaMalloc( &ctx->d_counter, sizeof( unsigned int ) ) );
 		SLAB_CUDA( cudaMemset( ctx->d_counter, 0, sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaDeviceSynchronize() ); // the memsets ran on the legacy stream
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_start ) );
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_stop ) );
+		SLAB_CUDA( cudaEventCreate( &ctx->solve_start ) );
+		SLAB_CUDA( cudaEventCreate( &ctx->solve_stop ) );
 		ensure_partials( ctx.get(), 4096 );
 		ensure_pinned( ctx.get(), 1024 );
 		*out = ctx.release();
@@ -126,6 +134,8 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		if( ctx->h_pinned ) cudaFreeHost( ctx->h_pinned );
 		cudaEventDestroy( ctx->timer_start );
 		cudaEventDestroy( ctx->timer_stop );
+		cudaEventDestroy( ctx->solve_start );
+		cudaEventDestroy( ctx->solve_stop );
 		cudaStreamDestroy( ctx->stream );
 		delete ctx;
 	} );
@@ -442,7 +452,7 @@ int slab_mask_create( slab_ctx_t ctx, uint64_t universe, const uint64_t * member
 		m->count = count;
 		SLAB_CUDA( cudaMalloc( &m->d_members, std::max< uint64_t >( count, 1 ) * sizeof( int32_t ) ) );
 		if( count > 0 ) {
-			SLAB_CUDA( cudaMemcpy( m->d_members, m32.data(), count * sizeof( int32_t ), cudaMemcpyHostToDevice ) );
+			upload_sync( ctx->stream, m->d_members, m32.data(), count * sizeof( int32_t ) );
 		}
 		*out = m.release();
 	} );
@@ -602,6 +612,7 @@ int slab_level_color_members( slab_level_t level, uint64_t k, uint64_t * members
 		need( members, "slab_level_color_members" );
 		bind( level->ctx );
 		std::vector< int32_t > rows( size );
+		SLAB_CUDA( cudaStreamSynchronize( level->ctx->stream ) );
 		SLAB_CUDA( cudaMemcpy( rows.data(), level->d_rows + level->color_pos[ k ], size * sizeof( int32_t ),
 			cudaMemcpyDeviceToHost ) );
 		for( uint64_t q = 0; q < size; ++q ) {

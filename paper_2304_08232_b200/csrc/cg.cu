@@ -109,7 +109,7 @@ namespace slabgpu {
 		CgWorkspace * ws = workspace( H, planned );
 		slab_vec_s * r = ws->r.get();
 
-		SLAB_CUDA( cudaEventRecord( ctx->timer_start, st ) );
+		SLAB_CUDA( cudaEventRecord( ctx->solve_start, st ) );
 		if( x->d != x0->d ) { // out.solution = x0, cg.hpp:91
 			SLAB_CUDA( cudaMemcpyAsync( x->d, x0->d, n * sizeof( double ), cudaMemcpyDeviceToDevice, st ) );
 		}
@@ -200,7 +200,7 @@ namespace slabgpu {
 				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + limit, ws->d_hist_pq, limit * sizeof( double ),
 					cudaMemcpyDeviceToHost, st ) );
 			}
-			SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
+			SLAB_CUDA( cudaEventRecord( ctx->solve_stop, st ) );
 			SLAB_CUDA( cudaStreamSynchronize( st ) );
 			for( uint64_t k = 0; k < limit; ++k ) {
 				if( ctx->h_pinned[ limit + k ] <= 0.0 ) { // cg.hpp:124-126
@@ -228,11 +228,11 @@ namespace slabgpu {
 					break;
 				}
 			}
-			SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
+			SLAB_CUDA( cudaEventRecord( ctx->solve_stop, st ) );
 			SLAB_CUDA( cudaStreamSynchronize( st ) );
 		}
 		float ms = 0.0f;
-		SLAB_CUDA( cudaEventElapsedTime( &ms, ctx->timer_start, ctx->timer_stop ) );
+		SLAB_CUDA( cudaEventElapsedTime( &ms, ctx->solve_start, ctx->solve_stop ) );
 		if( result ) {
 			result->iterations = count - 1;
 			result->converged = r_norm / denom < cfg->rtol ? 1 : 0;

@@ -40,7 +40,19 @@ namespace slabgpu {
 	}
 #define SLAB_CUDA( expr ) ::slabgpu::cuda_check( ( expr ), #expr, __FILE__, __LINE__ )
 
+	// Host -> device copy ordered on `stream` and complete on return. (A plain cudaMemcpy from
+	// pageable memory may return before the DMA has landed and is only ordered against the legacy
+	// stream, which the library's non-blocking streams do not synchronise with.)
+	inline void upload_sync( cudaStream_t stream, void * dst, const void * src, size_t bytes ) {
+		if( bytes == 0 ) {
+			return;
+		}
+		SLAB_CUDA( cudaMemcpyAsync( dst, src, bytes, cudaMemcpyHostToDevice, stream ) );
+		SLAB_CUDA( cudaStreamSynchronize( stream ) );
+	}
+
 	extern uint64_t g_launch_count;
+	extern int g_use_pdl; // chain kernels with programmatic dependent launch (default on)
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
 	}
@@ -83,7 +95,8 @@ struct slab_ctx_s {
 	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
 	double * h_pinned = nullptr;    // pinned staging for scalar read-back
 	uint64_t h_pinned_cap = 0;
-	cudaEvent_t timer_start = nullptr, timer_stop = nullptr;
+	cudaEvent_t timer_start = nullptr, timer_stop = nullptr; // slab_ctx_timer_* (caller-owned interval)
+	cudaEvent_t solve_start = nullptr, solve_stop = nullptr; // cg_solve's own interval (slab_cg_result::solve_ms)
 };
 
 struct slab_vec_s {

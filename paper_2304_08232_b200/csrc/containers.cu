@@ -77,7 +77,8 @@ namespace slabgpu {
 	namespace {
 
 		// uploads slice widths -> offsets, allocates vals/cols. Returns the host offsets.
-		std::vector< int64_t > sell_allocate( Sell & S, int64_t nrows, const std::vector< int32_t > & widths ) {
+		std::vector< int64_t > sell_allocate( cudaStream_t st, Sell & S, int64_t nrows,
+			const std::vector< int32_t > & widths ) {
 			S.nrows = nrows;
 			S.nslices = static_cast< int64_t >( widths.size() );
 			std::vector< int64_t > off( widths.size() + 1, 0 );
@@ -88,7 +89,7 @@ namespace slabgpu {
 			SLAB_CUDA( cudaMalloc( &S.slice_off, off.size() * sizeof( int64_t ) ) );
 			SLAB_CUDA( cudaMalloc( &S.vals, std::max< int64_t >( S.entries, 1 ) * sizeof( double ) ) );
 			SLAB_CUDA( cudaMalloc( &S.cols, std::max< int64_t >( S.entries, 1 ) * sizeof( int32_t ) ) );
-			SLAB_CUDA( cudaMemcpy( S.slice_off, off.data(), off.size() * sizeof( int64_t ), cudaMemcpyHostToDevice ) );
+			upload_sync( st, S.slice_off, off.data(), off.size() * sizeof( int64_t ) );
 			return off;
 		}
 
@@ -96,7 +97,6 @@ namespace slabgpu {
 
 	Sell sell_from_csr_rows( slab_ctx_s * ctx, const std::vector< int64_t > & rows, const uint64_t * ro,
 		const uint64_t * co, const double * va ) {
-		(void) ctx;
 		Sell S;
 		const int64_t npos = static_cast< int64_t >( rows.size() );
 		const int64_t nslices = ( npos + kSlice - 1 ) / kSlice;
@@ -108,7 +108,7 @@ namespace slabgpu {
 			}
 		}
 		try {
-			const std::vector< int64_t > off = sell_allocate( S, npos, widths );
+			const std::vector< int64_t > off = sell_allocate( ctx->stream, S, npos, widths );
 			std::vector< double > vals( std::max< int64_t >( S.entries, 1 ), 0.0 );
 			std::vector< int32_t > cols( std::max< int64_t >( S.entries, 1 ), -1 );
 			for( int64_t p = 0; p < npos; ++p ) {
@@ -123,8 +123,8 @@ namespace slabgpu {
 					cols[ base + static_cast< int64_t >( k - begin ) * kSlice ] = static_cast< int32_t >( co[ k ] );
 				}
 			}
-			SLAB_CUDA( cudaMemcpy( S.vals, vals.data(), S.entries * sizeof( double ), cudaMemcpyHostToDevice ) );
-			SLAB_CUDA( cudaMemcpy( S.cols, cols.data(), S.entries * sizeof( int32_t ), cudaMemcpyHostToDevice ) );
+			upload_sync( ctx->stream, S.vals, vals.data(), S.entries * sizeof( double ) );
+			upload_sync( ctx->stream, S.cols, cols.data(), S.entries * sizeof( int32_t ) );
 		} catch( ... ) {
 			S.release();
 			throw;
@@ -145,7 +145,7 @@ namespace slabgpu {
 			SLAB_CUDA( cudaMemcpyAsync( widths.data(), d_widths, nslices * sizeof( int32_t ), cudaMemcpyDeviceToHost,
 				ctx->stream ) );
 			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
-			sell_allocate( S, npos, widths );
+			sell_allocate( ctx->stream, S, npos, widths );
 			kern::stencil_fill( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
 				d_rows, npos, nslices, S.slice_off, S.vals, S.cols );
 			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
@@ -233,7 +233,7 @@ namespace slabgpu {
 		R->nnz = R->nrows;
 		const int64_t nslices = ( static_cast< int64_t >( R->nrows ) + kSlice - 1 ) / kSlice;
 		std::vector< int32_t > widths( nslices, 1 );
-		sell_allocate( R->sell, static_cast< int64_t >( R->nrows ), widths );
+		sell_allocate( ctx->stream, R->sell, static_cast< int64_t >( R->nrows ), widths );
 		int32_t * d_fine = nullptr;
 		SLAB_CUDA( cudaMalloc( &d_fine, std::max< uint64_t >( R->nrows, 1 ) * sizeof( int32_t ) ) );
 		kern::injection_cols( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
@@ -275,7 +275,7 @@ namespace slabgpu {
 			SLAB_CUDA( cudaMalloc( &d_off, ( nrows + 1 ) * sizeof( int64_t ) ) );
 			SLAB_CUDA( cudaMalloc( &d_cols, std::max< uint64_t >( A->nnz, 1 ) * sizeof( int64_t ) ) );
 			SLAB_CUDA( cudaMalloc( &d_vals, std::max< uint64_t >( A->nnz, 1 ) * sizeof( double ) ) );
-			SLAB_CUDA( cudaMemcpy( d_off, ro, ( nrows + 1 ) * sizeof( int64_t ), cudaMemcpyHostToDevice ) );
+			upload_sync( ctx->stream, d_off, ro, ( nrows + 1 ) * sizeof( int64_t ) );
 			kern::sell_to_csr( ctx->stream, A->sell.slice_off, A->sell.vals, A->sell.cols, nrows, d_off, d_cols, d_vals );
 			SLAB_CUDA( cudaMemcpyAsync( co, d_cols, A->nnz * sizeof( int64_t ), cudaMemcpyDeviceToHost, ctx->stream ) );
 			SLAB_CUDA( cudaMemcpyAsync( va, d_vals, A->nnz * sizeof( double ), cudaMemcpyDeviceToHost, ctx->stream ) );

@@ -5,9 +5,16 @@
 // arithmetic below goes through __dmul_rn/__dadd_rn/__ddiv_rn, which the compiler never
 // contracts, and the file is additionally built with -fmad=false.
 //
-// All kernels are HBM-bound streaming kernels: the matrix is read once, coalesced, with a
-// streaming (evict-first) hint so that it does not push the vectors out of the 126 MB L2; the
-// vector gathers are served by L1/L2.
+// Performance shape. Every kernel here is an HBM-bound (fine level) or latency-bound (coarse
+// levels) streaming kernel; none has GEMM shape, so no tensor-core path exists.
+//  * The matrix stream of a row (values + 32-bit columns, 12 B per stored entry) is immutable, so
+//    a thread issues ALL of its matrix loads up front, with a streaming (evict-first) hint that keeps
+//    the 126 MB L2 for the vectors. That gives each thread ~324 B in flight.
+//  * Kernels are chained with programmatic dependent launch: a kernel's blocks become resident
+//    and preload their matrix rows while the previous kernel drains; `griddepcontrol.wait` then
+//    orders every access to mutable data (vectors, scalars) after the previous kernel's writes.
+//    EVERY kernel executes the wait before touching mutable memory, so ordering is transitive.
+//  * Vector gathers (x / z) are served by L1/L2.
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -17,27 +24,123 @@
 namespace slabgpu {
 
 	uint64_t g_launch_count = 0;
+	int g_use_pdl = 1;
+	// launches with at least this many rows use the streaming kernels, smaller ones the preload
+	// kernels (about one full wave of 148 SMs x 2048 threads)
+	int64_t g_stream_rows = 262144;
 
 	namespace kern {
 
 		namespace {
 
 			constexpr int kBlock = 256;
+			constexpr int kChunk = 27; // slots preloaded per row in one go (a full 27-point row)
 
 			inline unsigned int blocks_for( uint64_t count, int block = kBlock ) {
 				return static_cast< unsigned int >( ( count + block - 1 ) / block );
 			}
 
-			// ordered row sum over one SELL row: acc = acc + val*x[col], stored entries only,
-			// ascending column order (operations.hpp:116-125). `diag_row` >= 0 also extracts
-			// the stored diagonal (problem.hpp:143-166) on the way.
+			// launch with the programmatic-stream-serialization attribute (PDL)
+			template< class... KArgs, class... Args >
+			void launch( void ( *kernel )( KArgs... ), unsigned int grid, unsigned int block, cudaStream_t st,
+				Args... args ) {
+				cudaLaunchConfig_t cfg{};
+				cfg.gridDim = dim3( grid, 1, 1 );
+				cfg.blockDim = dim3( block, 1, 1 );
+				cfg.dynamicSmemBytes = 0;
+				cfg.stream = st;
+				cudaLaunchAttribute attr[ 1 ];
+				attr[ 0 ].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+				attr[ 0 ].val.programmaticStreamSerializationAllowed = 1;
+				cfg.attrs = attr;
+				cfg.numAttrs = g_use_pdl ? 1 : 0;
+				SLAB_CUDA( cudaLaunchKernelEx( &cfg, kernel, static_cast< KArgs >( args )... ) );
+				count_launch();
+			}
+
+			// wait until the previous kernel in the stream has completed and its writes are visible
+			__device__ __forceinline__ void dep_wait() {
+				asm volatile( "griddepcontrol.wait;" ::: "memory" );
+			}
+			// let the next kernel's blocks be scheduled as soon as SM resources free up
+			__device__ __forceinline__ void dep_trigger() {
+				asm volatile( "griddepcontrol.launch_dependents;" ::: "memory" );
+			}
+
+			// ------------------------------------------------------------ SELL row access
+
+			struct RowChunk {
+				double v[ kChunk ];
+				int32_t c[ kChunk ];
+			};
+
+			// entries [first, first+count) of the row at position `pos`: issue all loads, no use yet
+			__device__ __forceinline__ void chunk_load( const double * __restrict__ vals, const int32_t * __restrict__ cols,
+				int64_t at, int count, RowChunk & rc ) {
+				#pragma unroll
+				for( int k = 0; k < kChunk; ++k ) {
+					if( k < count ) {
+						rc.c[ k ] = __ldcs( cols + at + static_cast< int64_t >( k ) * kSlice );
+						rc.v[ k ] = __ldcs( vals + at + static_cast< int64_t >( k ) * kSlice );
+					} else {
+						rc.c[ k ] = -1;
+						rc.v[ k ] = 0.0;
+					}
+				}
+			}
+
+			// ordered accumulation acc = acc + v*x[c] over the chunk's stored entries, ascending
+			// column order (operations.hpp:116-125); padding slots (c < 0) are skipped. All gathers
+			// are issued before the dependent add chain starts.
 			template< bool WANT_DIAG >
-			__device__ __forceinline__ double sell_row_sum( const int64_t * __restrict__ slice_off,
+			__device__ __forceinline__ double chunk_accumulate( const RowChunk & rc, int count, const double * x, double acc,
+				int32_t diag_row, double & diag ) {
+				constexpr int kBatch = 9; // gathers in flight per thread while the add chain runs
+				#pragma unroll
+				for( int k0 = 0; k0 < kChunk; k0 += kBatch ) {
+					double xv[ kBatch ];
+					#pragma unroll
+					for( int j = 0; j < kBatch; ++j ) {
+						const int k = k0 + j;
+						xv[ j ] = k < count ? x[ rc.c[ k ] < 0 ? 0 : rc.c[ k ] ] : 0.0;
+					}
+					#pragma unroll
+					for( int j = 0; j < kBatch; ++j ) {
+						const int k = k0 + j;
+						if( k < count ) {
+							const double sum = __dadd_rn( acc, __dmul_rn( rc.v[ k ], xv[ j ] ) );
+							acc = rc.c[ k ] < 0 ? acc : sum;
+							if( WANT_DIAG ) {
+								diag = rc.c[ k ] == diag_row ? rc.v[ k ] : diag;
+							}
+						}
+					}
+				}
+				return acc;
+			}
+
+			// rows wider than one chunk (general matrices): remaining chunks, loaded after the wait
+			template< bool WANT_DIAG >
+			__device__ __forceinline__ double row_tail( const double * __restrict__ vals, const int32_t * __restrict__ cols,
+				int64_t begin, int width, const double * x, double acc, int32_t diag_row, double & diag ) {
+				for( int k0 = kChunk; k0 < width; k0 += kChunk ) {
+					RowChunk rc;
+					const int count = width - k0 < kChunk ? width - k0 : kChunk;
+					chunk_load( vals, cols, begin + static_cast< int64_t >( k0 ) * kSlice, count, rc );
+					acc = chunk_accumulate< WANT_DIAG >( rc, count, x, acc, diag_row, diag );
+				}
+				return acc;
+			}
+
+			// Streaming form of the same ordered row sum for launches of many waves: a short rolling
+			// window of loads per thread (32 registers, 64 resident warps per SM) sustains more HBM
+			// bandwidth than the preload form, whose strength is the latency-bound small launch.
+			template< bool WANT_DIAG >
+			__device__ __forceinline__ double row_sum_streaming( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, int64_t pos, const double * x,
 				int32_t diag_row, double & diag ) {
 				const int64_t s = pos >> 5;
-				const int lane = static_cast< int >( pos & 31 );
-				const int64_t begin = slice_off[ s ] + lane;
+				const int64_t begin = slice_off[ s ] + ( pos & 31 );
 				const int64_t end = slice_off[ s + 1 ];
 				double acc = 0.0;
 				#pragma unroll 9
@@ -57,6 +160,8 @@ namespace slabgpu {
 			// ------------------------------------------------------------ vector ops
 
 			__global__ void k_fill( double * __restrict__ v, uint64_t n, double value ) {
+				dep_trigger();
+				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( i < n ) {
 					v[ i ] = value;
@@ -66,6 +171,8 @@ namespace slabgpu {
 			// operations.hpp:103 — w may alias x or y: each thread reads its inputs before writing
 			__global__ void k_waxpby( double * w, double alpha, const double * x, double beta, const double * y,
 				uint64_t n ) {
+				dep_trigger();
+				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( i < n ) {
 					const double ax = __dmul_rn( alpha, x[ i ] );
@@ -80,6 +187,8 @@ namespace slabgpu {
 			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * __restrict__ x,
 				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
 				__shared__ double prod[ kDotChunk ];
+				dep_trigger();
+				dep_wait();
 				const uint64_t begin = static_cast< uint64_t >( blockIdx.x ) * kDotChunk;
 				const uint64_t remaining = n - begin;
 				const int len = static_cast< int >( remaining < kDotChunk ? remaining : kDotChunk );
@@ -110,6 +219,8 @@ namespace slabgpu {
 			}
 
 			__global__ void k_dot_empty( double * out ) {
+				dep_trigger();
+				dep_wait();
 				*out = 0.0;
 			}
 
@@ -138,24 +249,16 @@ namespace slabgpu {
 				return v; // valid in thread 0
 			}
 
-			__global__ void __launch_bounds__( kBlock ) k_dot_tree( const double * __restrict__ x,
-				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
-				__shared__ double smem[ 32 ];
-				__shared__ bool is_last;
-				double acc = 0.0;
-				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
-				for( uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x; i < n; i += stride ) {
-					acc = __dadd_rn( acc, __dmul_rn( x[ i ], y[ i ] ) );
-				}
-				acc = block_tree_sum( acc, smem );
+			__device__ __forceinline__ void grid_tree_finish( double block_sum, double * partials, unsigned int * counter,
+				double * out, double * smem, bool * is_last ) {
 				if( threadIdx.x == 0 ) {
-					partials[ blockIdx.x ] = acc;
+					partials[ blockIdx.x ] = block_sum;
 					__threadfence();
 					const unsigned int ticket = atomicAdd( counter, 1u );
-					is_last = ticket == gridDim.x - 1;
+					*is_last = ticket == gridDim.x - 1;
 				}
 				__syncthreads();
-				if( is_last ) {
+				if( *is_last ) {
 					__threadfence();
 					double v = 0.0;
 					for( unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x ) {
@@ -169,50 +272,93 @@ namespace slabgpu {
 				}
 			}
 
-			// ------------------------------------------------------------ SELL products
-
-			__global__ void __launch_bounds__( kBlock ) k_spmv( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, int64_t nrows ) {
-				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( row >= nrows ) {
-					return;
+			__global__ void __launch_bounds__( kBlock ) k_dot_tree( const double * __restrict__ x,
+				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
+				__shared__ double smem[ 32 ];
+				__shared__ bool is_last;
+				dep_trigger();
+				dep_wait();
+				double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				for( ; i + 3 * stride < n; i += 4 * stride ) { // four independent loads in flight per thread
+					const double a0 = x[ i ], b0 = y[ i ];
+					const double a1 = x[ i + stride ], b1 = y[ i + stride ];
+					const double a2 = x[ i + 2 * stride ], b2 = y[ i + 2 * stride ];
+					const double a3 = x[ i + 3 * stride ], b3 = y[ i + 3 * stride ];
+					acc0 = __dadd_rn( acc0, __dmul_rn( a0, b0 ) );
+					acc1 = __dadd_rn( acc1, __dmul_rn( a1, b1 ) );
+					acc2 = __dadd_rn( acc2, __dmul_rn( a2, b2 ) );
+					acc3 = __dadd_rn( acc3, __dmul_rn( a3, b3 ) );
 				}
-				double unused = 0.0;
-				y[ row ] = sell_row_sum< false >( slice_off, vals, cols, row, x, -1, unused );
+				for( ; i < n; i += stride ) {
+					acc0 = __dadd_rn( acc0, __dmul_rn( x[ i ], y[ i ] ) );
+				}
+				const double acc = __dadd_rn( __dadd_rn( acc0, acc1 ), __dadd_rn( acc2, acc3 ) );
+				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, out, smem, &is_last );
 			}
 
-			__global__ void __launch_bounds__( kBlock ) k_spmv_masked( const int64_t * __restrict__ slice_off,
+			// ------------------------------------------------------------ SELL products
+
+			// operations.hpp:164-174. MASKED: one thread per mask member, others untouched.
+			template< bool MASKED >
+			__global__ void __launch_bounds__( kBlock ) k_spmv( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
 				double * __restrict__ y, const int32_t * __restrict__ members, int64_t count ) {
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( k >= count ) {
+				const bool live = k < count;
+				int64_t row = 0, begin = 0;
+				int width = 0;
+				RowChunk rc;
+				if( live ) {
+					row = MASKED ? members[ k ] : k;
+					const int64_t s = row >> 5;
+					const int64_t b = slice_off[ s ];
+					width = static_cast< int >( ( slice_off[ s + 1 ] - b ) >> 5 );
+					begin = b + ( row & 31 );
+					chunk_load( vals, cols, begin, width < kChunk ? width : kChunk, rc );
+				}
+				dep_trigger();
+				dep_wait();
+				if( !live ) {
 					return;
 				}
-				const int64_t row = members[ k ];
 				double unused = 0.0;
-				y[ row ] = sell_row_sum< false >( slice_off, vals, cols, row, x, -1, unused );
+				double acc = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, x, 0.0, -1, unused );
+				acc = row_tail< false >( vals, cols, begin, width, x, acc, -1, unused );
+				y[ row ] = acc;
 			}
 
 			// smoother.hpp:60-72 fused: s = row sum over z, then z[i] = ((r[i] - s) + z[i]*d) / d.
 			// Rows of one colour never neighbour each other, so reading z while other threads of
 			// the same launch write their own z[i] is race-free (coloring.hpp:165-204).
-			__global__ void __launch_bounds__( kBlock ) k_gs_color( const int64_t * __restrict__ slice_off,
+			__global__ void __launch_bounds__( kBlock, 2 ) k_gs_color( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( k >= pos_count ) {
-					return;
+				int32_t i = -1;
+				int64_t begin = 0;
+				int width = 0;
+				RowChunk rc;
+				if( k < pos_count ) {
+					const int64_t pos = pos_begin + k;
+					i = rows[ pos ];
+					const int64_t s = pos >> 5;
+					const int64_t b = slice_off[ s ];
+					width = static_cast< int >( ( slice_off[ s + 1 ] - b ) >> 5 );
+					begin = b + ( pos & 31 );
+					chunk_load( vals, cols, begin, width < kChunk ? width : kChunk, rc );
 				}
-				const int64_t pos = pos_begin + k;
-				const int32_t i = rows[ pos ];
+				dep_trigger();
+				dep_wait();
 				if( i < 0 ) {
 					return;
 				}
-				double d = 0.0;
-				const double s = sell_row_sum< true >( slice_off, vals, cols, pos, z, i, d );
-				const double zi = z[ i ];
 				const double ri = r[ i ];
+				double d = 0.0;
+				double s = chunk_accumulate< true >( rc, width < kChunk ? width : kChunk, z, 0.0, i, d );
+				s = row_tail< true >( vals, cols, begin, width, z, s, i, d );
+				const double zi = z[ i ];
 				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
 			}
 
@@ -223,12 +369,80 @@ namespace slabgpu {
 				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
 				double * __restrict__ r_c ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const bool live = p < n_coarse;
+				int32_t i = 0;
+				int64_t begin = 0;
+				int width = 0;
+				RowChunk rc;
+				if( live ) {
+					i = rows[ p ];
+					const int64_t s = p >> 5;
+					const int64_t b = slice_off[ s ];
+					width = static_cast< int >( ( slice_off[ s + 1 ] - b ) >> 5 );
+					begin = b + ( p & 31 );
+					chunk_load( vals, cols, begin, width < kChunk ? width : kChunk, rc );
+				}
+				dep_trigger();
+				dep_wait();
+				if( !live ) {
+					return;
+				}
+				double unused = 0.0;
+				double az = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, z, 0.0, -1, unused );
+				az = row_tail< false >( vals, cols, begin, width, z, az, -1, unused );
+				const double f = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -1.0, az ) );
+				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+			}
+
+			// ---- streaming forms (many-wave launches on the fine level); same arithmetic, same order
+
+			__global__ void __launch_bounds__( kBlock ) k_spmv_stream( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
+				double * __restrict__ y, int64_t nrows ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( row >= nrows ) {
+					return;
+				}
+				double unused = 0.0;
+				y[ row ] = row_sum_streaming< false >( slice_off, vals, cols, row, x, -1, unused );
+			}
+
+			__global__ void __launch_bounds__( kBlock ) k_gs_color_stream( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( k >= pos_count ) {
+					return;
+				}
+				const int64_t pos = pos_begin + k;
+				const int32_t i = rows[ pos ];
+				if( i < 0 ) {
+					return;
+				}
+				double d = 0.0;
+				const double s = row_sum_streaming< true >( slice_off, vals, cols, pos, z, i, d );
+				const double zi = z[ i ];
+				const double ri = r[ i ];
+				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+			}
+
+			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_stream( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
+				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
+				double * __restrict__ r_c ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( p >= n_coarse ) {
 					return;
 				}
 				const int32_t i = rows[ p ];
 				double unused = 0.0;
-				const double az = sell_row_sum< false >( slice_off, vals, cols, p, z, -1, unused );
+				const double az = row_sum_streaming< false >( slice_off, vals, cols, p, z, -1, unused );
 				const double f = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -1.0, az ) );
 				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 			}
@@ -238,10 +452,12 @@ namespace slabgpu {
 			__global__ void k_prolong_add( const int32_t * __restrict__ rows, int64_t n_coarse, double * z,
 				const double * __restrict__ z_c ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( p >= n_coarse ) {
+				const int32_t i = p < n_coarse ? rows[ p ] : -1;
+				dep_trigger();
+				dep_wait();
+				if( i < 0 ) {
 					return;
 				}
-				const int32_t i = rows[ p ];
 				const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, z_c[ p ] ) );
 				z[ i ] = __dadd_rn( __dmul_rn( 1.0, z[ i ] ), __dmul_rn( 1.0, f ) );
 			}
@@ -250,6 +466,8 @@ namespace slabgpu {
 
 			__global__ void k_cg_update_p( double * p, const double * __restrict__ z, const double * __restrict__ scalars,
 				const unsigned int * __restrict__ iter_counter, uint64_t n ) {
+				dep_trigger();
+				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( i >= n ) {
 					return;
@@ -257,7 +475,7 @@ namespace slabgpu {
 				const double zi = z[ i ];
 				if( *iter_counter == 0u ) { // cg.hpp:118  waxpby( p, 1.0, z, 0.0, z )
 					p[ i ] = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 0.0, zi ) );
-				} else {      // cg.hpp:120  waxpby( p, 1.0, z, rho / rho_prev, p )
+				} else {                    // cg.hpp:120  waxpby( p, 1.0, z, rho / rho_prev, p )
 					const double beta = __ddiv_rn( scalars[ S_RHO ], scalars[ S_RHO_PREV ] );
 					p[ i ] = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( beta, p[ i ] ) );
 				}
@@ -265,6 +483,8 @@ namespace slabgpu {
 
 			__global__ void k_cg_update_xr( double * x, double * r, const double * __restrict__ p,
 				const double * __restrict__ q, double * scalars, uint64_t n ) {
+				dep_trigger();
+				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const double rho = scalars[ S_RHO ];
 				const double alpha = __ddiv_rn( rho, scalars[ S_PQ ] ); // cg.hpp:127
@@ -279,143 +499,12 @@ namespace slabgpu {
 
 			__global__ void k_cg_record( const double * __restrict__ scalars, double * hist_rr, double * hist_pq,
 				unsigned int * iter_counter ) {
+				dep_trigger();
+				dep_wait();
 				const unsigned int it = *iter_counter;
 				hist_rr[ it ] = scalars[ S_RR ];
 				hist_pq[ it ] = scalars[ S_PQ ];
 				*iter_counter = it + 1;
-			}
-
-			// ------------------------------------------------------------ setup kernels
-
-			__device__ __forceinline__ int span( int i, int n ) {
-				return ( i > 0 ? 1 : 0 ) + 1 + ( i + 1 < n ? 1 : 0 );
-			}
-
-			__global__ void k_stencil_widths( int nx, int ny, int nz, const int32_t * __restrict__ rows, int64_t npos,
-				int64_t nslices, int32_t * __restrict__ widths ) {
-				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( ( pos >> 5 ) >= nslices ) {
-					return;
-				}
-				int count = 0;
-				if( pos < npos ) {
-					const int64_t i = rows ? rows[ pos ] : pos;
-					if( i >= 0 ) {
-						const int ix = static_cast< int >( i % nx );
-						const int iy = static_cast< int >( ( i / nx ) % ny );
-						const int iz = static_cast< int >( i / ( static_cast< int64_t >( nx ) * ny ) );
-						count = span( ix, nx ) * span( iy, ny ) * span( iz, nz );
-					}
-				}
-				const int width = __reduce_max_sync( 0xffffffffu, count );
-				if( ( threadIdx.x & 31 ) == 0 ) {
-					widths[ pos >> 5 ] = width;
-				}
-			}
-
-			// problem.hpp:108-127: neighbours ascend lexicographically in (z,y,x), 26 on the
-			// diagonal and -1 off it; remaining slots of the slice are padding (col -1).
-			__global__ void k_stencil_fill( int nx, int ny, int nz, const int32_t * __restrict__ rows, int64_t npos,
-				int64_t nslices, const int64_t * __restrict__ slice_off, double * __restrict__ vals,
-				int32_t * __restrict__ cols ) {
-				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				const int64_t s = pos >> 5;
-				if( s >= nslices ) {
-					return;
-				}
-				int64_t e = slice_off[ s ] + ( pos & 31 );
-				const int64_t end = slice_off[ s + 1 ];
-				const int64_t i = pos < npos ? ( rows ? rows[ pos ] : pos ) : -1;
-				if( i >= 0 ) {
-					const int ix = static_cast< int >( i % nx );
-					const int iy = static_cast< int >( ( i / nx ) % ny );
-					const int iz = static_cast< int >( i / ( static_cast< int64_t >( nx ) * ny ) );
-					for( int jz = iz > 0 ? iz - 1 : 0; jz < nz && jz <= iz + 1; ++jz ) {
-						for( int jy = iy > 0 ? iy - 1 : 0; jy < ny && jy <= iy + 1; ++jy ) {
-							for( int jx = ix > 0 ? ix - 1 : 0; jx < nx && jx <= ix + 1; ++jx ) {
-								const int64_t j = jx + static_cast< int64_t >( nx ) * ( jy + static_cast< int64_t >( ny ) * jz );
-								vals[ e ] = j == i ? 26.0 : -1.0;
-								cols[ e ] = static_cast< int32_t >( j );
-								e += kSlice;
-							}
-						}
-					}
-				}
-				for( ; e < end; e += kSlice ) {
-					vals[ e ] = 0.0;
-					cols[ e ] = -1;
-				}
-			}
-
-			__global__ void k_color_rows( int nx, int ny, int px, int py, int pz, int sx, int sy, int64_t pos0, int64_t size,
-				int64_t padded, int32_t * __restrict__ rows ) {
-				const int64_t q = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( q >= padded ) {
-					return;
-				}
-				int32_t out = -1;
-				if( q < size ) {
-					const int cx = static_cast< int >( q % sx );
-					const int cy = static_cast< int >( ( q / sx ) % sy );
-					const int cz = static_cast< int >( q / ( static_cast< int64_t >( sx ) * sy ) );
-					out = static_cast< int32_t >( ( 2 * cx + px )
-						+ static_cast< int64_t >( nx ) * ( ( 2 * cy + py ) + static_cast< int64_t >( ny ) * ( 2 * cz + pz ) ) );
-				}
-				rows[ pos0 + q ] = out;
-			}
-
-			__global__ void k_injection_cols( int nx, int ny, int cxn, int cyn, int64_t nc, int32_t * __restrict__ fine ) {
-				const int64_t c = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( c >= nc ) {
-					return;
-				}
-				const int cx = static_cast< int >( c % cxn );
-				const int cy = static_cast< int >( ( c / cxn ) % cyn );
-				const int cz = static_cast< int >( c / ( static_cast< int64_t >( cxn ) * cyn ) );
-				fine[ c ] = static_cast< int32_t >( 2 * cx + static_cast< int64_t >( nx ) * ( 2 * cy + static_cast< int64_t >( ny ) * 2 * cz ) );
-			}
-
-			__global__ void k_sell_single_entry( const int32_t * __restrict__ col_of_row, int64_t nrows, int64_t nslices,
-				double * __restrict__ vals, int32_t * __restrict__ cols ) {
-				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( ( pos >> 5 ) >= nslices ) {
-					return;
-				}
-				const bool live = pos < nrows;
-				vals[ pos ] = live ? 1.0 : 0.0;
-				cols[ pos ] = live ? col_of_row[ pos ] : -1;
-			}
-
-			__global__ void k_sell_row_counts( const int64_t * __restrict__ slice_off, const int32_t * __restrict__ cols,
-				int64_t nrows, int64_t * __restrict__ counts ) {
-				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( row >= nrows ) {
-					return;
-				}
-				const int64_t s = row >> 5;
-				int64_t count = 0;
-				for( int64_t e = slice_off[ s ] + ( row & 31 ); e < slice_off[ s + 1 ]; e += kSlice ) {
-					count += cols[ e ] >= 0 ? 1 : 0;
-				}
-				counts[ row ] = count;
-			}
-
-			__global__ void k_sell_to_csr( const int64_t * __restrict__ slice_off, const double * __restrict__ vals,
-				const int32_t * __restrict__ cols, int64_t nrows, const int64_t * __restrict__ row_off,
-				int64_t * __restrict__ out_cols, double * __restrict__ out_vals ) {
-				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( row >= nrows ) {
-					return;
-				}
-				const int64_t s = row >> 5;
-				int64_t at = row_off[ row ];
-				for( int64_t e = slice_off[ s ] + ( row & 31 ); e < slice_off[ s + 1 ]; e += kSlice ) {
-					if( cols[ e ] >= 0 ) {
-						out_cols[ at ] = cols[ e ];
-						out_vals[ at ] = vals[ e ];
-						++at;
-					}
-				}
 			}
 
 		} // namespace
@@ -426,8 +515,7 @@ namespace slabgpu {
 			if( n == 0 ) {
 				return;
 			}
-			k_fill<<< blocks_for( n ), kBlock, 0, st >>>( v, n, value );
-			count_launch();
+			launch( k_fill, blocks_for( n ), kBlock, st, v, n, value );
 		}
 
 		void waxpby( cudaStream_t st, double * w, double alpha, const double * x, double beta, const double * y,
@@ -435,25 +523,22 @@ namespace slabgpu {
 			if( n == 0 ) {
 				return;
 			}
-			k_waxpby<<< blocks_for( n ), kBlock, 0, st >>>( w, alpha, x, beta, y, n );
-			count_launch();
+			launch( k_waxpby, blocks_for( n ), kBlock, st, w, alpha, x, beta, y, n );
 		}
 
 		void dot_exact( cudaStream_t st, const double * x, const double * y, uint64_t n, double * partials,
 			unsigned int * counter, double * out ) {
 			if( n == 0 ) {
-				k_dot_empty<<< 1, 1, 0, st >>>( out );
-				count_launch();
+				launch( k_dot_empty, 1, 1, st, out );
 				return;
 			}
 			const unsigned int nchunks = static_cast< unsigned int >( ( n + kDotChunk - 1 ) / kDotChunk );
-			k_dot_exact<<< nchunks, 32, 0, st >>>( x, y, n, partials, counter, out );
-			count_launch();
+			launch( k_dot_exact, nchunks, 32, st, x, y, n, partials, counter, out );
 		}
 
 		uint64_t dot_tree_blocks( uint64_t n, int sm_count ) {
-			const uint64_t want = ( n + kBlock * 8 - 1 ) / ( kBlock * 8 );
-			const uint64_t cap = static_cast< uint64_t >( sm_count ) * 4;
+			const uint64_t want = ( n + kBlock * 4 - 1 ) / ( kBlock * 4 );
+			const uint64_t cap = static_cast< uint64_t >( sm_count ) * 8;
 			const uint64_t blocks = want < cap ? want : cap;
 			return blocks < 1 ? 1 : blocks;
 		}
@@ -461,13 +546,11 @@ namespace slabgpu {
 		void dot_tree( cudaStream_t st, const double * x, const double * y, uint64_t n, int sm_count, double * partials,
 			unsigned int * counter, double * out ) {
 			if( n == 0 ) {
-				k_dot_empty<<< 1, 1, 0, st >>>( out );
-				count_launch();
+				launch( k_dot_empty, 1, 1, st, out );
 				return;
 			}
 			const unsigned int blocks = static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) );
-			k_dot_tree<<< blocks, kBlock, 0, st >>>( x, y, n, partials, counter, out );
-			count_launch();
+			launch( k_dot_tree, blocks, kBlock, st, x, y, n, partials, counter, out );
 		}
 
 		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
@@ -475,8 +558,12 @@ namespace slabgpu {
 			if( nrows == 0 ) {
 				return;
 			}
-			k_spmv<<< blocks_for( nrows ), kBlock, 0, st >>>( slice_off, vals, cols, x, y, nrows );
-			count_launch();
+			if( nrows >= g_stream_rows ) {
+				launch( k_spmv_stream, blocks_for( nrows ), kBlock, st, slice_off, vals, cols, x, y, nrows );
+				return;
+			}
+			launch( k_spmv< false >, blocks_for( nrows ), kBlock, st, slice_off, vals, cols, x, y,
+				static_cast< const int32_t * >( nullptr ), nrows );
 		}
 
 		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
@@ -484,8 +571,7 @@ namespace slabgpu {
 			if( count == 0 ) {
 				return;
 			}
-			k_spmv_masked<<< blocks_for( count ), kBlock, 0, st >>>( slice_off, vals, cols, x, y, members, count );
-			count_launch();
+			launch( k_spmv< true >, blocks_for( count ), kBlock, st, slice_off, vals, cols, x, y, members, count );
 		}
 
 		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
@@ -493,9 +579,13 @@ namespace slabgpu {
 			if( pos_count == 0 ) {
 				return;
 			}
-			k_gs_color<<< blocks_for( pos_count ), kBlock, 0, st >>>( slice_off, vals, cols, rows, pos_begin, pos_count, z,
+			if( pos_count >= g_stream_rows ) {
+				launch( k_gs_color_stream, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin,
+					pos_count, z, r );
+				return;
+			}
+			launch( k_gs_color, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z,
 				r );
-			count_launch();
 		}
 
 		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
@@ -503,17 +593,20 @@ namespace slabgpu {
 			if( n_coarse == 0 ) {
 				return;
 			}
-			k_residual_restrict<<< blocks_for( n_coarse ), kBlock, 0, st >>>( slice_off, vals, cols, rows, n_coarse, z, r,
+			if( n_coarse >= g_stream_rows ) {
+				launch( k_residual_restrict_stream, blocks_for( n_coarse ), kBlock, st, slice_off, vals, cols, rows, n_coarse,
+					z, r, r_c );
+				return;
+			}
+			launch( k_residual_restrict, blocks_for( n_coarse ), kBlock, st, slice_off, vals, cols, rows, n_coarse, z, r,
 				r_c );
-			count_launch();
 		}
 
 		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c ) {
 			if( n_coarse == 0 ) {
 				return;
 			}
-			k_prolong_add<<< blocks_for( n_coarse ), kBlock, 0, st >>>( rows, n_coarse, z, z_c );
-			count_launch();
+			launch( k_prolong_add, blocks_for( n_coarse ), kBlock, st, rows, n_coarse, z, z_c );
 		}
 
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,
@@ -521,90 +614,17 @@ namespace slabgpu {
 			if( n == 0 ) {
 				return;
 			}
-			k_cg_update_p<<< blocks_for( n ), kBlock, 0, st >>>( p, z, scalars, iter_counter, n );
-			count_launch();
+			launch( k_cg_update_p, blocks_for( n ), kBlock, st, p, z, scalars, iter_counter, n );
 		}
 
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n ) {
-			k_cg_update_xr<<< n == 0 ? 1 : blocks_for( n ), kBlock, 0, st >>>( x, r, p, q, scalars, n );
-			count_launch();
+			launch( k_cg_update_xr, n == 0 ? 1u : blocks_for( n ), kBlock, st, x, r, p, q, scalars, n );
 		}
 
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,
 			unsigned int * iter_counter ) {
-			k_cg_record<<< 1, 1, 0, st >>>( scalars, hist_rr, hist_pq, iter_counter );
-			count_launch();
-		}
-
-		void stencil_widths( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
-			int32_t * widths ) {
-			if( nslices == 0 ) {
-				return;
-			}
-			k_stencil_widths<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( nx, ny, nz, rows, npos, nslices, widths );
-			count_launch();
-		}
-
-		void stencil_fill( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
-			const int64_t * slice_off, double * vals, int32_t * cols ) {
-			if( nslices == 0 ) {
-				return;
-			}
-			k_stencil_fill<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( nx, ny, nz, rows, npos, nslices, slice_off,
-				vals, cols );
-			count_launch();
-		}
-
-		void color_rows( cudaStream_t st, int nx, int ny, int nz, int px, int py, int pz, int64_t pos0, int64_t size,
-			int64_t padded, int32_t * rows ) {
-			(void) nz;
-			if( padded == 0 ) {
-				return;
-			}
-			const int sx = ( nx + 1 - px ) / 2;
-			const int sy = ( ny + 1 - py ) / 2;
-			k_color_rows<<< blocks_for( padded ), kBlock, 0, st >>>( nx, ny, px, py, pz, sx > 0 ? sx : 1, sy > 0 ? sy : 1,
-				pos0, size, padded, rows );
-			count_launch();
-		}
-
-		void injection_cols( cudaStream_t st, int nx, int ny, int nz, int32_t * fine ) {
-			const int64_t nc = static_cast< int64_t >( nx / 2 ) * ( ny / 2 ) * ( nz / 2 );
-			if( nc == 0 ) {
-				return;
-			}
-			k_injection_cols<<< blocks_for( nc ), kBlock, 0, st >>>( nx, ny, nx / 2, ny / 2, nc, fine );
-			count_launch();
-		}
-
-		void sell_single_entry( cudaStream_t st, const int32_t * col_of_row, int64_t nrows, int64_t nslices, double * vals,
-			int32_t * cols ) {
-			if( nslices == 0 ) {
-				return;
-			}
-			k_sell_single_entry<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( col_of_row, nrows, nslices, vals,
-				cols );
-			count_launch();
-		}
-
-		void sell_row_counts( cudaStream_t st, const int64_t * slice_off, const int32_t * cols, int64_t nrows,
-			int64_t * counts ) {
-			if( nrows == 0 ) {
-				return;
-			}
-			k_sell_row_counts<<< blocks_for( nrows ), kBlock, 0, st >>>( slice_off, cols, nrows, counts );
-			count_launch();
-		}
-
-		void sell_to_csr( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			int64_t nrows, const int64_t * row_off, int64_t * out_cols, double * out_vals ) {
-			if( nrows == 0 ) {
-				return;
-			}
-			k_sell_to_csr<<< blocks_for( nrows ), kBlock, 0, st >>>( slice_off, vals, cols, nrows, row_off, out_cols,
-				out_vals );
-			count_launch();
+			launch( k_cg_record, 1, 1, st, scalars, hist_rr, hist_pq, iter_counter );
 		}
 
 	} // namespace kern

@@ -216,9 +216,9 @@ namespace slabgpu {
 		L->colorA = sell_from_csr_rows( ctx, rows, ro, co, va );
 		std::vector< int32_t > rows32( rows.begin(), rows.end() );
 		SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< size_t >( rows32.size(), 1 ) * sizeof( int32_t ) ) );
-		SLAB_CUDA( cudaMemcpy( L->d_rows, rows32.data(), rows32.size() * sizeof( int32_t ), cudaMemcpyHostToDevice ) );
+		upload_sync( ctx->stream, L->d_rows, rows32.data(), rows32.size() * sizeof( int32_t ) );
 		L->a_diag.reset( vec_new( ctx, n, 0.0 ) );
-		SLAB_CUDA( cudaMemcpy( L->a_diag->d, diag.data(), n * sizeof( double ), cudaMemcpyHostToDevice ) );
+		upload_sync( ctx->stream, L->a_diag->d, diag.data(), n * sizeof( double ) );
 		alloc_scratch( L.get(), 0 );
 		return L.release();
 	}
