@@ -68,6 +68,9 @@ const char * slab_status_name( int status );
 uint64_t slab_launch_count( void );
 /* chain kernels with programmatic dependent launch (griddepcontrol): 1 (default) or 0. Process-wide. */
 int slab_set_programmatic_launch( int enabled );
+/* performance knobs that never change results: "stream_rows" (launches with at least this many rows
+ * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl". Process-wide. */
+int slab_set_tuning( const char * key, int64_t value );
 
 /* ------------------------------------------------------------------ context */
 int slab_ctx_create( int device, slab_ctx_t * out );

@@ -98,6 +98,7 @@ SIGNATURES = {
     "slab_status_name": (C.c_char_p, [C.c_int]),
     "slab_launch_count": (_u64, []),
     "slab_set_programmatic_launch": (C.c_int, [C.c_int]),
+    "slab_set_tuning": (C.c_int, [C.c_char_p, C.c_int64]),
     "slab_ctx_create": (C.c_int, [C.c_int, _pvp]),
     "slab_ctx_destroy": (C.c_int, [_vp]),
     "slab_ctx_sync": (C.c_int, [_vp]),
@@ -183,6 +184,11 @@ def _check(rc: int) -> None:
 
 def set_programmatic_launch(enabled: bool) -> None:
     _check(load_library().slab_set_programmatic_launch(int(enabled)))
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Performance knobs that never change results (see slab_set_tuning in include/slab_b200.h)."""
+    _check(load_library().slab_set_tuning(key.encode(), int(value)))
 
 
 def launch_count() -> int:

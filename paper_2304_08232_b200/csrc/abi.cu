@@ -1,5 +1,6 @@
 // abi.cu — the extern "C" surface declared in include/slab_b200.h. Every entry point
 // translates internal exceptions into status codes; argument checks precede any work.
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -73,6 +74,22 @@ int slab_set_programmatic_launch( int enabled ) {
 	return SLAB_OK;
 }
 
+int slab_set_tuning( const char * key, int64_t value ) {
+	return guarded( [ & ] {
+		need( key, "slab_set_tuning" );
+		const std::string k( key );
+		if( k == "stream_rows" ) {
+			g_stream_rows = value;
+		} else if( k == "stream_variant" ) {
+			g_stream_variant = static_cast< int >( value );
+		} else if( k == "pdl" ) {
+			g_use_pdl = value ? 1 : 0;
+		} else {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "slab_set_tuning: unknown key " + k );
+		}
+	} );
+}
+
 uint64_t slab_launch_count( void ) {
 	return g_launch_count;
 }
@@ -98,6 +115,16 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		if( prop.major < 10 ) {
 			fail( SLAB_ERR_CUDA, std::string( "device " ) + prop.name + " is sm_" + std::to_string( prop.major )
 				+ std::to_string( prop.minor ) + "; this library is built for sm_100a only" );
+		}
+		// performance knobs from the environment (never change results; see slab_set_tuning)
+		if( const char * v = std::getenv( "SLAB_PDL" ) ) {
+			g_use_pdl = std::atoi( v ) ? 1 : 0;
+		}
+		if( const char * v = std::getenv( "SLAB_STREAM_ROWS" ) ) {
+			g_stream_rows = std::atoll( v );
+		}
+		if( const char * v = std::getenv( "SLAB_STREAM_VARIANT" ) ) {
+			g_stream_variant = std::atoi( v );
 		}
 		std::unique_ptr< slab_ctx_s > ctx( new slab_ctx_s );
 		ctx->device = device;

@@ -51,6 +51,8 @@ namespace slabgpu {
 		SLAB_CUDA( cudaStreamSynchronize( stream ) );
 	}
 
+	extern int64_t g_stream_rows;
+	extern int g_stream_variant;
 	extern uint64_t g_launch_count;
 	extern int g_use_pdl; // chain kernels with programmatic dependent launch (default on)
 	inline void count_launch( uint64_t k = 1 ) {

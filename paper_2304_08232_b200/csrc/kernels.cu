@@ -26,8 +26,11 @@ namespace slabgpu {
 	uint64_t g_launch_count = 0;
 	int g_use_pdl = 1;
 	// launches with at least this many rows use the streaming kernels, smaller ones the preload
-	// kernels (about one full wave of 148 SMs x 2048 threads)
-	int64_t g_stream_rows = 262144;
+	// kernels (measured cross-over on B200: ~1e5 rows, a third of a full wave of 148 SMs x 2048 threads)
+	int64_t g_stream_rows = 100000;
+	// which streaming kernel shape the many-wave launches use (tuning knob). 2 = batches of 9 slots,
+	// 48 registers, 40 resident warps per SM: best of the sweep in profiles/r01_microbench_*.json
+	int g_stream_variant = 2;
 
 	namespace kern {
 
@@ -394,6 +397,96 @@ namespace slabgpu {
 				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 			}
 
+			// Batched streaming row sum: B (column, value) pairs are loaded together, then their B
+			// gathers, then the B-long ordered add chain; the next batch's matrix loads are issued
+			// before the chain of the current one runs (software pipelining by hand).
+			template< int B, bool WANT_DIAG >
+			__device__ __forceinline__ double row_sum_batched( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, int64_t pos, const double * x,
+				int32_t diag_row, double & diag ) {
+				const int64_t s = pos >> 5;
+				const int64_t base = slice_off[ s ];
+				const int width = static_cast< int >( ( slice_off[ s + 1 ] - base ) >> 5 );
+				const double * vp = vals + base + ( pos & 31 );
+				const int32_t * cp = cols + base + ( pos & 31 );
+				double acc = 0.0;
+				int32_t c[ B ];
+				double v[ B ];
+				#pragma unroll
+				for( int j = 0; j < B; ++j ) {
+					const bool in = j < width;
+					c[ j ] = in ? __ldcs( cp + j * kSlice ) : -1;
+					v[ j ] = in ? __ldcs( vp + j * kSlice ) : 0.0;
+				}
+				for( int k0 = 0; k0 < width; k0 += B ) {
+					double xv[ B ];
+					#pragma unroll
+					for( int j = 0; j < B; ++j ) {
+						xv[ j ] = x[ c[ j ] < 0 ? 0 : c[ j ] ];
+					}
+					int32_t cc[ B ];
+					double vv[ B ];
+					#pragma unroll
+					for( int j = 0; j < B; ++j ) {
+						cc[ j ] = c[ j ];
+						vv[ j ] = v[ j ];
+					}
+					// next batch of matrix entries goes out before the dependent chain below
+					#pragma unroll
+					for( int j = 0; j < B; ++j ) {
+						const int k = k0 + B + j;
+						const bool in = k < width;
+						c[ j ] = in ? __ldcs( cp + k * kSlice ) : -1;
+						v[ j ] = in ? __ldcs( vp + k * kSlice ) : 0.0;
+					}
+					#pragma unroll
+					for( int j = 0; j < B; ++j ) {
+						const double sum = __dadd_rn( acc, __dmul_rn( vv[ j ], xv[ j ] ) );
+						acc = cc[ j ] < 0 ? acc : sum;
+						if( WANT_DIAG ) {
+							diag = cc[ j ] == diag_row ? vv[ j ] : diag;
+						}
+					}
+				}
+				return acc;
+			}
+
+			template< int B, int MINBLOCKS >
+			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_batched( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( k >= pos_count ) {
+					return;
+				}
+				const int64_t pos = pos_begin + k;
+				const int32_t i = rows[ pos ];
+				if( i < 0 ) {
+					return;
+				}
+				double d = 0.0;
+				const double s = row_sum_batched< B, true >( slice_off, vals, cols, pos, z, i, d );
+				const double zi = z[ i ];
+				const double ri = r[ i ];
+				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+			}
+
+			template< int B, int MINBLOCKS >
+			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_spmv_batched( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
+				double * __restrict__ y, int64_t nrows ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( row >= nrows ) {
+					return;
+				}
+				double unused = 0.0;
+				y[ row ] = row_sum_batched< B, false >( slice_off, vals, cols, row, x, -1, unused );
+			}
+
 			// ---- streaming forms (many-wave launches on the fine level); same arithmetic, same order
 
 			__global__ void __launch_bounds__( kBlock ) k_spmv_stream( const int64_t * __restrict__ slice_off,
@@ -559,7 +652,26 @@ namespace slabgpu {
 				return;
 			}
 			if( nrows >= g_stream_rows ) {
-				launch( k_spmv_stream, blocks_for( nrows ), kBlock, st, slice_off, vals, cols, x, y, nrows );
+				const unsigned int grid = blocks_for( nrows );
+				switch( g_stream_variant ) {
+					case 1:
+						launch( k_spmv_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						break;
+					case 2:
+						launch( k_spmv_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						break;
+					case 3:
+						launch( k_spmv_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						break;
+					case 4:
+						launch( k_spmv_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						break;
+					case 5:
+						launch( k_spmv_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						break;
+					default:
+						launch( k_spmv_stream, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+				}
 				return;
 			}
 			launch( k_spmv< false >, blocks_for( nrows ), kBlock, st, slice_off, vals, cols, x, y,
@@ -580,8 +692,29 @@ namespace slabgpu {
 				return;
 			}
 			if( pos_count >= g_stream_rows ) {
-				launch( k_gs_color_stream, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin,
-					pos_count, z, r );
+				const unsigned int grid = blocks_for( pos_count );
+				switch( g_stream_variant ) {
+					case 1:
+						launch( k_gs_color_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					case 2:
+						launch( k_gs_color_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					case 3:
+						launch( k_gs_color_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					case 4:
+						launch( k_gs_color_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					case 5:
+						launch( k_gs_color_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					case 6:
+						launch( k_gs_color, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						break;
+					default:
+						launch( k_gs_color_stream, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+				}
 				return;
 			}
 			launch( k_gs_color, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z,

@@ -1,0 +1,99 @@
+"""CPU tests (no GPU): the C-ABI library builds for sm_100a, loads, and exports every symbol that
+include/slab_b200.h declares; the Python mirror types all of them; and without a GPU the product
+path fails loudly instead of falling back to anything.
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "slab_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(slab_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_reference_operator_surface():
+    names = set(declared_functions())
+    for required in ["slab_mxv", "slab_mxv_masked", "slab_dot", "slab_waxpby", "slab_set_all", "slab_rbgs_color_step",
+                     "slab_rbgs_forward", "slab_rbgs_backward", "slab_rbgs_symmetric", "slab_restrict_vector",
+                     "slab_refine_and_add", "slab_mg_vcycle", "slab_cg_solve", "slab_cg_solve_host",
+                     "slab_residual_norm", "slab_hierarchy_create", "slab_level_create_csr", "slab_mat_create_csr",
+                     "slab_mat_create_stencil27", "slab_mask_create", "slab_vec_upload", "slab_vec_download"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(slab):
+    lib = ctypes.CDLL(slab.LIB_PATH)
+    missing = [name for name in declared_functions() if not hasattr(lib, name)]
+    assert not missing, missing
+
+
+def test_python_mirror_types_every_declared_symbol(slab):
+    assert sorted(slab.SIGNATURES) == declared_functions()
+
+
+def test_library_is_built_for_sm_100a_only(slab):
+    out = subprocess.run(["cuobjdump", "--list-elf", slab.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump not available")
+    archs = set(re.findall(r"sm_\d+a?", out.stdout))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_status_names_follow_the_reference_error_taxonomy(slab):
+    lib = slab.load_library()
+    assert lib.slab_abi_version() == 1
+    assert lib.slab_status_name(1) == b"DimensionMismatch"   # error.hpp:30
+    assert lib.slab_status_name(2) == b"InvalidArgument"     # error.hpp:35
+    assert lib.slab_status_name(3) == b"SolverBreakdown"     # error.hpp:40
+
+
+def test_no_cpu_fallback_without_a_gpu(slab):
+    """On a box without a GPU creating a context must raise; on a GPU box it must succeed."""
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        slab.Context(0)
+        return
+    with pytest.raises(slab.CudaError) as info:
+        slab.Context(0)
+    assert "no CPU fallback" in str(info.value)
+
+
+def test_product_never_imports_the_oracle():
+    """oracle/ is test infrastructure: nothing under the package may reference it."""
+    pkg = os.path.join(ROOT, "paper_2304_08232_b200")
+    offenders = []
+    for base, _dirs, files in os.walk(pkg):
+        for name in files:
+            if name.endswith((".py", ".cu", ".cuh", ".hpp", ".h")):
+                text = open(os.path.join(base, name)).read()
+                if re.search(r"import\s+oracle|from\s+oracle|slab_oracle|libslab_ref|oracle/|\bso_[a-z_]+\s*\(", text):
+                    offenders.append(os.path.join(base, name))
+    assert not offenders, offenders
+
+
+def test_bench_counting_matches_survey_denominators():
+    """per-iteration flops and fused-minimum bytes used by bench.py."""
+    import bench
+
+    assert bench.hpcg_flops_per_iteration((64, 64, 64)) == pytest.approx(94.78e6, rel=2e-4)
+    assert bench.hpcg_flops_per_iteration((104, 104, 104)) == pytest.approx(412.1e6, rel=2e-4)
+    assert bench.hpcg_flops_per_iteration((192, 192, 192)) == pytest.approx(2.618e9, rel=2e-4)
+    assert bench.algorithmic_bytes_per_iteration((64, 64, 64)) == pytest.approx(0.5438e9, rel=2e-3)
+    assert bench.algorithmic_bytes_per_iteration((104, 104, 104)) == pytest.approx(2.361e9, rel=2e-3)
+    assert bench.algorithmic_bytes_per_iteration((192, 192, 192)) == pytest.approx(14.98e9, rel=2e-3)
+    n, nnz = 256 ** 3, 766 ** 3
+    assert 8 * bench.gs_step_bytes((256, 256, 256)) * 2 == 2 * (12 * nnz + 32 * n)  # 11.861 GB per symmetric sweep
+    assert np.isclose(2 * (12 * nnz + 32 * n), 11.861e9, rtol=1e-3)
