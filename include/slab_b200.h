@@ -192,6 +192,33 @@ int slab_cg_solve_host( slab_level_t hierarchy, const double * b, const double *
 /* residual_norm cg.hpp:59-67 */
 int slab_residual_norm( slab_mat_t A, slab_vec_t x, slab_vec_t b, double * out );
 
+/* ------------------------------------------------------------------ 3D domain decomposition (no reference
+ * equivalent: distributed execution is out of the reference's scope; the paper's MPI "Ref" exchanges
+ * geometric halos per colour). One process per GPU. After slab_ctx_set_process_grid the dims
+ * given to slab_hierarchy_create are the LOCAL grid of this rank; the global grid is local x process grid, every
+ * level is decomposed the same way, colours and column order follow GLOBAL coordinates so that per-row
+ * arithmetic is identical to the single-process solve on the global grid. Vectors created on such a context
+ * carry a ghost tail; create them after the hierarchy. dot() returns the sum over ranks once a communicator is
+ * attached. Direction index = (dz+1)*9 + (dy+1)*3 + (dx+1). */
+int slab_ctx_set_process_grid( slab_ctx_t ctx, int px, int py, int pz, int rank ); /* rank = rx + px*(ry + py*rz) */
+int slab_nccl_unique_id( unsigned char * out128 );                /* rank 0 creates it, everybody gets a copy */
+int slab_ctx_init_nccl( slab_ctx_t ctx, const unsigned char * id128 ); /* collective: ncclCommInitRank */
+int slab_ctx_dist_info( slab_ctx_t ctx, int grid[ 3 ], int * rank, int * nranks, int * has_comm, uint64_t * exchanges );
+int slab_level_decomp( slab_level_t level, uint64_t global_dims[ 3 ], uint64_t offset[ 3 ], uint64_t * n_ghost );
+/* manual halo access (no communicator attached): what a custom transport or a test moves between ranks.
+ * colour -1 = all colours of that direction. pack gathers this rank's boundary values into host_out;
+ * unpack stores a peer's packed values into the ghost range of v. */
+int slab_level_halo_info( slab_level_t level, int dir, int color, uint64_t * send_count, uint64_t * recv_count, int * peer );
+int slab_level_halo_pack( slab_level_t level, slab_vec_t v, int dir, int color, double * host_out );
+int slab_level_halo_unpack( slab_level_t level, slab_vec_t v, int dir, int color, const double * host_in );
+/* host-only view of the halo plan of any rank (runs without a GPU): counts, peer, first ghost slot and the
+ * local indices of the send list of (direction, colour); and the local (owned or ghost) index of a global point */
+int slab_plan_query( const uint64_t local_dims[ 3 ], const uint64_t grid[ 3 ], uint64_t rank, int dir, int color,
+	uint64_t * n_local, uint64_t * n_ghost, uint64_t * send_count, uint64_t * recv_count, int64_t * peer,
+	uint64_t * ghost_base, uint64_t * send_indices );
+int slab_plan_local_index( const uint64_t local_dims[ 3 ], const uint64_t grid[ 3 ], uint64_t rank, uint64_t X, uint64_t Y,
+	uint64_t Z, int64_t * out );
+
 #ifdef __cplusplus
 }
 #endif

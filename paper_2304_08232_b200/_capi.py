@@ -154,6 +154,19 @@ SIGNATURES = {
     "slab_cg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(_CgConfig), _vp, _vp, C.POINTER(_CgResult)]),
     "slab_cg_solve_host": (C.c_int, [_vp, _vp, _vp, _u64, C.POINTER(_CgConfig), _vp, _vp, C.POINTER(_CgResult)]),
     "slab_residual_norm": (C.c_int, [_vp, _vp, _vp, _pf64]),
+    "slab_ctx_set_process_grid": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "slab_nccl_unique_id": (C.c_int, [_vp]),
+    "slab_ctx_init_nccl": (C.c_int, [_vp, _vp]),
+    "slab_ctx_dist_info": (C.c_int, [_vp, C.POINTER(C.c_int * 3), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int), _pu64]),
+    "slab_level_decomp": (C.c_int, [_vp, C.POINTER(C.c_uint64 * 3), C.POINTER(C.c_uint64 * 3), _pu64]),
+    "slab_level_halo_info": (C.c_int, [_vp, C.c_int, C.c_int, _pu64, _pu64, C.POINTER(C.c_int)]),
+    "slab_level_halo_pack": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "slab_level_halo_unpack": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "slab_plan_query": (C.c_int, [C.POINTER(C.c_uint64 * 3), C.POINTER(C.c_uint64 * 3), _u64, C.c_int, C.c_int, _pu64,
+                                  _pu64, _pu64, _pu64, C.POINTER(C.c_int64), _pu64, _vp]),
+    "slab_plan_local_index": (C.c_int, [C.POINTER(C.c_uint64 * 3), C.POINTER(C.c_uint64 * 3), _u64, _u64, _u64, _u64,
+                                        C.POINTER(C.c_int64)]),
 }
 
 _lib = None
@@ -189,6 +202,36 @@ def set_programmatic_launch(enabled: bool) -> None:
 def set_tuning(key: str, value: int) -> None:
     """Performance knobs that never change results (see slab_set_tuning in include/slab_b200.h)."""
     _check(load_library().slab_set_tuning(key.encode(), int(value)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(load_library().slab_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def plan_query(local_dims, grid, rank: int, direction: int, color: int) -> dict:
+    """Host-only halo plan of one rank for (direction, colour); needs no GPU."""
+    lib = load_library()
+    ld = (C.c_uint64 * 3)(*[int(v) for v in local_dims])
+    pg = (C.c_uint64 * 3)(*[int(v) for v in grid])
+    nl, ng, sc, rc, gb = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    peer = C.c_int64()
+    _check(lib.slab_plan_query(C.byref(ld), C.byref(pg), rank, direction, color, C.byref(nl), C.byref(ng), C.byref(sc),
+                               C.byref(rc), C.byref(peer), C.byref(gb), None))
+    idx = np.empty(sc.value, dtype=np.uint64)
+    _check(lib.slab_plan_query(C.byref(ld), C.byref(pg), rank, direction, color, None, None, None, None, None, None,
+                               _ptr(idx)))
+    return {"n_local": nl.value, "n_ghost": ng.value, "send_count": sc.value, "recv_count": rc.value,
+            "peer": peer.value, "ghost_base": gb.value, "send_indices": idx}
+
+
+def plan_local_index(local_dims, grid, rank: int, X: int, Y: int, Z: int) -> int:
+    ld = (C.c_uint64 * 3)(*[int(v) for v in local_dims])
+    pg = (C.c_uint64 * 3)(*[int(v) for v in grid])
+    out = C.c_int64()
+    _check(load_library().slab_plan_local_index(C.byref(ld), C.byref(pg), rank, X, Y, Z, C.byref(out)))
+    return out.value
 
 
 def launch_count() -> int:
@@ -259,6 +302,22 @@ class Context:
         sm, ma, mi, mem = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
         _check(_lib.slab_ctx_device_info(self._h, C.byref(sm), C.byref(ma), C.byref(mi), C.byref(mem)))
         return {"sm_count": sm.value, "cc": (ma.value, mi.value), "hbm_bytes": mem.value}
+
+    # ---- 3D domain decomposition (one process per GPU)
+    def set_process_grid(self, grid, rank: int) -> None:
+        _check(_lib.slab_ctx_set_process_grid(self._h, int(grid[0]), int(grid[1]), int(grid[2]), int(rank)))
+
+    def init_nccl(self, unique_id: bytes) -> None:
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        _check(_lib.slab_ctx_init_nccl(self._h, C.cast(buf, C.c_void_p)))
+
+    def dist_info(self) -> dict:
+        grid = (C.c_int * 3)()
+        rank, nranks, comm, ex = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
+        _check(_lib.slab_ctx_dist_info(self._h, C.byref(grid), C.byref(rank), C.byref(nranks), C.byref(comm),
+                                       C.byref(ex)))
+        return {"grid": tuple(grid), "rank": rank.value, "nranks": nranks.value, "has_comm": bool(comm.value),
+                "exchanges": ex.value}
 
     # factories in the reference's vocabulary
     def DenseVector(self, length_or_values, value: float = 0.0) -> "DenseVector":
@@ -560,6 +619,30 @@ class ProblemLevel:  # problem.hpp:220-277
 
     def reset_stats(self) -> None:
         _check(_lib.slab_level_stats_reset(self._h))
+
+    # ---- domain decomposition: manual halo access (tests, custom transports)
+    def decomp(self) -> dict:
+        g, o = (C.c_uint64 * 3)(), (C.c_uint64 * 3)()
+        ng = C.c_uint64()
+        _check(_lib.slab_level_decomp(self._h, C.byref(g), C.byref(o), C.byref(ng)))
+        return {"global": tuple(int(v) for v in g), "offset": tuple(int(v) for v in o), "n_ghost": ng.value}
+
+    def halo_info(self, direction: int, color: int = -1):
+        s, r, p = C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(_lib.slab_level_halo_info(self._h, direction, color, C.byref(s), C.byref(r), C.byref(p)))
+        return s.value, r.value, p.value
+
+    def halo_pack(self, v: DenseVector, direction: int, color: int = -1) -> np.ndarray:
+        count = self.halo_info(direction, color)[0]
+        out = np.empty(count, dtype=np.float64)
+        _check(_lib.slab_level_halo_pack(self._h, v._h, direction, color, _ptr(out)))
+        return out
+
+    def halo_unpack(self, v: DenseVector, direction: int, color: int, values: np.ndarray) -> None:
+        values = _f64(values)
+        if values.size != self.halo_info(direction, color)[1]:
+            raise DimensionMismatch("halo_unpack: message length differs from the ghost range")
+        _check(_lib.slab_level_halo_unpack(self._h, v._h, direction, color, _ptr(values)))
 
 
 # ---------------------------------------------------------------- operations.hpp

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libslab_b200.so")
 SOURCES = ["kernels.cu", "kernels_setup.cu", "containers.cu", "level.cu", "cg.cu", "dist.cu", "abi.cu"]
-HEADERS = ["common.hpp", "kernels.cuh", os.path.join("..", "..", "include", "slab_b200.h")]
+HEADERS = ["common.hpp", "kernels.cuh", "decomp.hpp", "dist.hpp", os.path.join("..", "..", "include", "slab_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -5,6 +5,7 @@
 #include <new>
 
 #include "common.hpp"
+#include "dist.hpp"
 #include "kernels.cuh"
 
 using namespace slabgpu;
@@ -155,6 +156,7 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		}
 		cudaSetDevice( ctx->device );
 		cudaStreamSynchronize( ctx->stream );
+		dist_destroy( ctx );
 		cudaFree( ctx->d_scalars );
 		cudaFree( ctx->d_partials );
 		cudaFree( ctx->d_counter );
@@ -793,6 +795,196 @@ int slab_residual_norm( slab_mat_t A, slab_vec_t x, slab_vec_t b, double * out )
 		same_ctx( A->ctx, b->ctx );
 		bind( A->ctx );
 		*out = residual_norm( A, x, b );
+	} );
+}
+
+// ---------------------------------------------------------------- domain decomposition
+
+int slab_ctx_set_process_grid( slab_ctx_t ctx, int px, int py, int pz, int rank ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_set_process_grid" );
+		dist_set_grid( ctx, px, py, pz, rank );
+	} );
+}
+
+int slab_nccl_unique_id( unsigned char * out128 ) {
+	return guarded( [ & ] {
+		need( out128, "slab_nccl_unique_id" );
+		NcclUniqueId id;
+		nccl_unique_id( &id );
+		std::memcpy( out128, id.internal, sizeof( id.internal ) );
+	} );
+}
+
+int slab_ctx_init_nccl( slab_ctx_t ctx, const unsigned char * id128 ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_init_nccl" );
+		need( id128, "slab_ctx_init_nccl" );
+		bind( ctx );
+		NcclUniqueId id;
+		std::memcpy( id.internal, id128, sizeof( id.internal ) );
+		dist_init_nccl( ctx, &id );
+	} );
+}
+
+int slab_ctx_dist_info( slab_ctx_t ctx, int grid[ 3 ], int * rank, int * nranks, int * has_comm, uint64_t * exchanges ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_dist_info" );
+		const DistState * d = ctx->dist;
+		if( grid ) {
+			for( int a = 0; a < 3; ++a ) {
+				grid[ a ] = d ? d->p[ a ] : 1;
+			}
+		}
+		if( rank ) *rank = d ? d->rank : 0;
+		if( nranks ) *nranks = d ? d->nranks : 1;
+		if( has_comm ) *has_comm = d && d->comm ? 1 : 0;
+		if( exchanges ) *exchanges = d ? d->exchanges : 0;
+	} );
+}
+
+int slab_level_decomp( slab_level_t level, uint64_t global_dims[ 3 ], uint64_t offset[ 3 ], uint64_t * n_ghost ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_decomp" );
+		for( int a = 0; a < 3; ++a ) {
+			if( global_dims ) global_dims[ a ] = static_cast< uint64_t >( level->decomp.g[ a ] );
+			if( offset ) offset[ a ] = static_cast< uint64_t >( level->decomp.o[ a ] );
+		}
+		if( n_ghost ) *n_ghost = static_cast< uint64_t >( level->decomp.n_ghost );
+	} );
+}
+
+namespace {
+	void halo_range( slab_level_s * level, int dir, int color, int & send_first, int & send_n, int & recv_first, int & recv_n ) {
+		if( level->plan == nullptr ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "level is not distributed" );
+		}
+		if( dir < 0 || dir >= 27 || color < -1 || color >= 8 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "halo: direction must be in [0,27), colour in [-1,8)" );
+		}
+		const HaloPlan * plan = level->plan;
+		const int c0 = color < 0 ? 0 : color, c1 = color < 0 ? 8 : color + 1;
+		send_first = plan->send_off[ dir ][ c0 ];
+		recv_first = plan->D.ghost_base[ dir ][ c0 ];
+		send_n = recv_n = 0;
+		for( int c = c0; c < c1; ++c ) {
+			send_n += plan->send_count[ dir ][ c ];
+			recv_n += plan->D.ghost_count[ dir ][ c ];
+		}
+	}
+} // namespace
+
+int slab_level_halo_info( slab_level_t level, int dir, int color, uint64_t * send_count, uint64_t * recv_count, int * peer ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_halo_info" );
+		int sf, sn, rf, rn;
+		halo_range( level, dir, color, sf, sn, rf, rn );
+		if( send_count ) *send_count = static_cast< uint64_t >( sn );
+		if( recv_count ) *recv_count = static_cast< uint64_t >( rn );
+		if( peer ) *peer = level->plan->peer[ dir ];
+	} );
+}
+
+int slab_level_halo_pack( slab_level_t level, slab_vec_t v, int dir, int color, double * host_out ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_halo_pack" );
+		need( v, "slab_level_halo_pack" );
+		int sf, sn, rf, rn;
+		halo_range( level, dir, color, sf, sn, rf, rn );
+		if( v->n != level->n ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "halo: vector length differs from the level size" );
+		}
+		if( sn == 0 ) {
+			return;
+		}
+		need( host_out, "slab_level_halo_pack" );
+		slab_ctx_s * ctx = level->ctx;
+		bind( ctx );
+		halo_pack( ctx, level->plan, v, color );
+		SLAB_CUDA( cudaMemcpyAsync( host_out, level->plan->d_sendbuf + sf, static_cast< size_t >( sn ) * sizeof( double ),
+			cudaMemcpyDeviceToHost, ctx->stream ) );
+		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+	} );
+}
+
+int slab_level_halo_unpack( slab_level_t level, slab_vec_t v, int dir, int color, const double * host_in ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_halo_unpack" );
+		need( v, "slab_level_halo_unpack" );
+		int sf, sn, rf, rn;
+		halo_range( level, dir, color, sf, sn, rf, rn );
+		if( v->n != level->n
+			|| v->n_alloc < static_cast< uint64_t >( level->decomp.n_local ) + static_cast< uint64_t >( level->decomp.n_ghost ) ) {
+			fail( SLAB_ERR_DIMENSION_MISMATCH, "halo: vector does not belong to this level (or predates the hierarchy)" );
+		}
+		if( rn == 0 ) {
+			return;
+		}
+		need( host_in, "slab_level_halo_unpack" );
+		bind( level->ctx );
+		upload_sync( level->ctx->stream, v->d + level->decomp.n_local + rf, host_in, static_cast< size_t >( rn ) * sizeof( double ) );
+	} );
+}
+
+// host-only: the halo plan of one rank, computed without touching a GPU
+int slab_plan_query( const uint64_t local_dims[ 3 ], const uint64_t grid[ 3 ], uint64_t rank, int dir, int color,
+	uint64_t * n_local, uint64_t * n_ghost, uint64_t * send_count, uint64_t * recv_count, int64_t * peer,
+	uint64_t * ghost_base, uint64_t * send_indices ) {
+	return guarded( [ & ] {
+		need( local_dims, "slab_plan_query" );
+		need( grid, "slab_plan_query" );
+		const int p[ 3 ] = { static_cast< int >( grid[ 0 ] ), static_cast< int >( grid[ 1 ] ), static_cast< int >( grid[ 2 ] ) };
+		const int l[ 3 ] = { static_cast< int >( local_dims[ 0 ] ), static_cast< int >( local_dims[ 1 ] ),
+			static_cast< int >( local_dims[ 2 ] ) };
+		if( p[ 0 ] < 1 || p[ 1 ] < 1 || p[ 2 ] < 1 || rank >= static_cast< uint64_t >( p[ 0 ] ) * p[ 1 ] * p[ 2 ] || dir < 0 || dir >= 27
+			|| color < 0 || color >= 8 ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "slab_plan_query: bad grid, rank, direction or colour" );
+		}
+		int r[ 3 ];
+		rank_coords( p, static_cast< int >( rank ), r );
+		const Decomp D = make_decomp( l, p, r );
+		const int d[ 3 ] = { dir % 3 - 1, ( dir / 3 ) % 3 - 1, dir / 9 - 1 };
+		const int nr[ 3 ] = { r[ 0 ] + d[ 0 ], r[ 1 ] + d[ 1 ], r[ 2 ] + d[ 2 ] };
+		const bool exists = dir != 13 && nr[ 0 ] >= 0 && nr[ 0 ] < p[ 0 ] && nr[ 1 ] >= 0 && nr[ 1 ] < p[ 1 ] && nr[ 2 ] >= 0
+			&& nr[ 2 ] < p[ 2 ];
+		std::vector< int32_t > list;
+		if( exists ) {
+			send_list( D, dir, color, list );
+		}
+		if( n_local ) *n_local = static_cast< uint64_t >( D.n_local );
+		if( n_ghost ) *n_ghost = static_cast< uint64_t >( D.n_ghost );
+		if( send_count ) *send_count = list.size();
+		if( recv_count ) *recv_count = static_cast< uint64_t >( D.ghost_count[ dir ][ color ] );
+		if( peer ) *peer = exists ? nr[ 0 ] + p[ 0 ] * ( nr[ 1 ] + p[ 1 ] * nr[ 2 ] ) : -1;
+		if( ghost_base ) *ghost_base = static_cast< uint64_t >( D.ghost_base[ dir ][ color ] );
+		if( send_indices ) {
+			for( size_t k = 0; k < list.size(); ++k ) {
+				send_indices[ k ] = static_cast< uint64_t >( list[ k ] );
+			}
+		}
+	} );
+}
+
+int slab_plan_local_index( const uint64_t local_dims[ 3 ], const uint64_t grid[ 3 ], uint64_t rank, uint64_t X, uint64_t Y,
+	uint64_t Z, int64_t * out ) {
+	return guarded( [ & ] {
+		need( local_dims, "slab_plan_local_index" );
+		need( grid, "slab_plan_local_index" );
+		need( out, "slab_plan_local_index" );
+		const int p[ 3 ] = { static_cast< int >( grid[ 0 ] ), static_cast< int >( grid[ 1 ] ), static_cast< int >( grid[ 2 ] ) };
+		const int l[ 3 ] = { static_cast< int >( local_dims[ 0 ] ), static_cast< int >( local_dims[ 1 ] ),
+			static_cast< int >( local_dims[ 2 ] ) };
+		int r[ 3 ];
+		rank_coords( p, static_cast< int >( rank ), r );
+		const Decomp D = make_decomp( l, p, r );
+		const int c[ 3 ] = { static_cast< int >( X ), static_cast< int >( Y ), static_cast< int >( Z ) };
+		for( int a = 0; a < 3; ++a ) { // only points within one layer of the owned box are addressable
+			if( c[ a ] < 0 || c[ a ] >= D.g[ a ] || c[ a ] < D.o[ a ] - 1 || c[ a ] > D.o[ a ] + D.l[ a ] ) {
+				*out = -1;
+				return;
+			}
+		}
+		*out = local_index( D, c[ 0 ], c[ 1 ], c[ 2 ] );
 	} );
 }
 

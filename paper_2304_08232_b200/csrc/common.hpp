@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/slab_b200.h"
+#include "decomp.hpp"
 
 namespace slabgpu {
 
@@ -79,10 +80,13 @@ namespace slabgpu {
 	};
 
 	struct CgWorkspace;
+	struct DistState; // dist.cu: process grid + NCCL communicator of a context
+	struct HaloPlan;  // dist.cu: per-level send lists / ghost layout
 
 } // namespace slabgpu
 
 struct slab_ctx_s {
+	slabgpu::DistState * dist = nullptr; // null: single-process context
 	int device = 0;
 	cudaStream_t stream = nullptr;
 	int sm_count = 0;
@@ -117,6 +121,7 @@ struct slab_mat_s {
 	slab_ctx_s * ctx = nullptr;
 	uint64_t nrows = 0, ncols = 0, nnz = 0;
 	slabgpu::Sell sell;             // natural row order
+	slabgpu::HaloPlan * plan = nullptr; // borrowed from the level: columns >= ncols are ghost slots
 	std::unique_ptr< slab_mat_s > transposed; // built lazily for SLAB_DESC_TRANSPOSE
 	// host CSR kept when the matrix came from slab_mat_create_csr (small, test-sized inputs)
 	std::vector< uint64_t > h_row_offsets, h_cols;
@@ -146,6 +151,8 @@ struct slab_level_s {
 	std::unique_ptr< slab_mat_s > A;       // natural-order SELL
 	slabgpu::Sell colorA;                  // colour-major SELL (positions)
 	int32_t * d_rows = nullptr;            // position -> natural row, -1 on padding
+	slabgpu::Decomp decomp{};              // owned box of this rank on this level (whole grid when not distributed)
+	slabgpu::HaloPlan * plan = nullptr;    // owned; null on single-process contexts and general levels
 	uint64_t num_colors = 0;
 	std::vector< int64_t > color_pos;      // first position of colour k (multiple of 32); size num_colors+1
 	std::vector< uint64_t > color_size;    // members per colour
@@ -193,6 +200,7 @@ namespace slabgpu {
 	slab_mat_s * mat_from_csr( slab_ctx_s * ctx, uint64_t nrows, uint64_t ncols, const uint64_t * ro,
 		const uint64_t * co, const double * va, bool validate );
 	slab_mat_s * mat_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz );
+	slab_mat_s * mat_stencil27_box( slab_ctx_s * ctx, const Decomp & D ); // rows of the owned box, ghost columns
 	slab_mat_s * mat_restriction( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz );
 	void mat_download_csr( slab_mat_s * A, uint64_t * ro, uint64_t * co, double * va );
 	slab_mat_s * mat_transposed( slab_mat_s * A );
@@ -200,8 +208,20 @@ namespace slabgpu {
 	Sell sell_from_csr_rows( slab_ctx_s * ctx, const std::vector< int64_t > & rows, const uint64_t * ro,
 		const uint64_t * co, const double * va );
 	// SELL of the 27-point stencil over an arbitrary device row list (d_rows == nullptr: natural order)
-	Sell sell_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, const int32_t * d_rows,
-		int64_t npos );
+	Sell sell_stencil27( slab_ctx_s * ctx, const Decomp & D, const int32_t * d_rows, int64_t npos );
+	Decomp single_domain( uint64_t nx, uint64_t ny, uint64_t nz );
+
+	// ---- dist.cu (3D domain decomposition, halo exchange, allreduce)
+	Decomp level_decomp( const slab_ctx_s * ctx, uint64_t lx, uint64_t ly, uint64_t lz ); // owned box of this rank
+	uint64_t ghost_capacity( const slab_ctx_s * ctx );
+	HaloPlan * halo_plan_create( slab_ctx_s * ctx, const Decomp & D );
+	void halo_plan_destroy( HaloPlan * plan );
+	// bring the ghost copies of v up to date: colour < 0 exchanges every colour. No-op on
+	// single-process contexts and in manual-exchange mode (no communicator attached).
+	void halo_exchange( slab_level_s * L, slab_vec_s * v, int color );
+	void halo_exchange_plan( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color );
+	void allreduce_slot( slab_ctx_s * ctx, int slot ); // sum d_scalars[slot] over ranks, in place
+	void dist_destroy( slab_ctx_s * ctx );
 
 	// ---- level.cu
 	slab_level_s * hierarchy_create( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t levels );

@@ -4,6 +4,7 @@
 #include <numeric>
 
 #include "common.hpp"
+#include "dist.hpp"
 #include "kernels.cuh"
 
 namespace slabgpu {
@@ -62,9 +63,13 @@ namespace slabgpu {
 		std::unique_ptr< slab_vec_s > v( new slab_vec_s );
 		v->ctx = ctx;
 		v->n = n;
-		v->n_alloc = n;
-		SLAB_CUDA( cudaMalloc( &v->d, std::max< uint64_t >( n, 1 ) * sizeof( double ) ) );
+		// on a distributed context every vector carries room for the ghost points of the finest level
+		v->n_alloc = n + ghost_capacity( ctx );
+		SLAB_CUDA( cudaMalloc( &v->d, std::max< uint64_t >( v->n_alloc, 1 ) * sizeof( double ) ) );
 		kern::fill( ctx->stream, v->d, n, value );
+		if( v->n_alloc > n ) {
+			kern::fill( ctx->stream, v->d + n, v->n_alloc - n, 0.0 );
+		}
 		return v.release();
 	}
 
@@ -132,22 +137,23 @@ namespace slabgpu {
 		return S;
 	}
 
-	Sell sell_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz, const int32_t * d_rows,
-		int64_t npos ) {
+	Decomp single_domain( uint64_t nx, uint64_t ny, uint64_t nz ) {
+		return single_domain_decomp( static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ) );
+	}
+
+	Sell sell_stencil27( slab_ctx_s * ctx, const Decomp & D, const int32_t * d_rows, int64_t npos ) {
 		Sell S;
 		const int64_t nslices = ( npos + kSlice - 1 ) / kSlice;
 		int32_t * d_widths = nullptr;
 		try {
 			SLAB_CUDA( cudaMalloc( &d_widths, std::max< int64_t >( nslices, 1 ) * sizeof( int32_t ) ) );
-			kern::stencil_widths( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
-				d_rows, npos, nslices, d_widths );
+			kern::stencil_widths( ctx->stream, D, d_rows, npos, nslices, d_widths );
 			std::vector< int32_t > widths( nslices );
 			SLAB_CUDA( cudaMemcpyAsync( widths.data(), d_widths, nslices * sizeof( int32_t ), cudaMemcpyDeviceToHost,
 				ctx->stream ) );
 			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
 			sell_allocate( ctx->stream, S, npos, widths );
-			kern::stencil_fill( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
-				d_rows, npos, nslices, S.slice_off, S.vals, S.cols );
+			kern::stencil_fill( ctx->stream, D, d_rows, npos, nslices, S.slice_off, S.vals, S.cols );
 			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
 		} catch( ... ) {
 			if( d_widths ) cudaFree( d_widths );
@@ -217,7 +223,33 @@ namespace slabgpu {
 		A->ctx = ctx;
 		A->nrows = A->ncols = nx * ny * nz;
 		A->nnz = ( 3 * nx - 2 ) * ( 3 * ny - 2 ) * ( 3 * nz - 2 ); // problem.hpp:80-82
-		A->sell = sell_stencil27( ctx, nx, ny, nz, nullptr, static_cast< int64_t >( A->nrows ) );
+		A->sell = sell_stencil27( ctx, single_domain( nx, ny, nz ), nullptr, static_cast< int64_t >( A->nrows ) );
+		return A.release();
+	}
+
+	// the rows a rank owns: n_local x n_local logical shape, columns >= n_local address ghost slots
+	slab_mat_s * mat_stencil27_box( slab_ctx_s * ctx, const Decomp & D ) {
+		for( int a = 0; a < 3; ++a ) {
+			if( D.l[ a ] < 2 ) { // problem.hpp:65-70, per rank
+				fail( SLAB_ERR_INVALID_ARGUMENT, "grid dimensions must all be at least 2" );
+			}
+		}
+		if( static_cast< uint64_t >( D.n_local ) + static_cast< uint64_t >( D.n_ghost ) >= ( uint64_t( 1 ) << 31 ) ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "grid too large for 32-bit column indices on one device" );
+		}
+		std::unique_ptr< slab_mat_s > A( new slab_mat_s );
+		A->ctx = ctx;
+		A->nrows = A->ncols = static_cast< uint64_t >( D.n_local );
+		uint64_t nnz = 1;
+		for( int a = 0; a < 3; ++a ) {
+			uint64_t sum = 0;
+			for( int t = D.o[ a ]; t < D.o[ a ] + D.l[ a ]; ++t ) {
+				sum += static_cast< uint64_t >( span_1d( t, D.g[ a ] ) );
+			}
+			nnz *= sum;
+		}
+		A->nnz = nnz; // equals (3nx-2)(3ny-2)(3nz-2) on a single domain (problem.hpp:80-82)
+		A->sell = sell_stencil27( ctx, D, nullptr, static_cast< int64_t >( A->nrows ) );
 		return A.release();
 	}
 
@@ -328,7 +360,9 @@ namespace slabgpu {
 	// ---------------------------------------------------------------- primitive ops
 
 	void op_set_all( slab_vec_s * v, double value ) {
-		kern::fill( v->ctx->stream, v->d, v->n, value );
+		// the ghost tail of a distributed vector mirrors the owners' values: a constant vector is
+		// constant everywhere, so filling the tail too keeps the ghost copies consistent
+		kern::fill( v->ctx->stream, v->d, v->n_alloc, value );
 	}
 
 	void op_waxpby( slab_vec_s * w, double alpha, slab_vec_s * x, double beta, slab_vec_s * y ) {
@@ -351,6 +385,7 @@ namespace slabgpu {
 			kern::dot_tree( ctx->stream, x->d, y->d, x->n, ctx->sm_count, ctx->d_partials, ctx->d_counter,
 				ctx->d_scalars + slot );
 		}
+		allreduce_slot( ctx, slot ); // sum of the ranks' owned parts; no-op on one process
 	}
 
 	double op_dot( slab_vec_s * x, slab_vec_s * y ) {
@@ -373,6 +408,9 @@ namespace slabgpu {
 		}
 		slab_mat_s * M = transpose ? mat_transposed( A ) : A;
 		cudaStream_t st = A->ctx->stream;
+		if( A->plan != nullptr && !transpose ) {
+			halo_exchange_plan( A->ctx, A->plan, x, -1 ); // ghost copies of x before the gather
+		}
 		if( mask == nullptr ) {
 			kern::spmv( st, M->sell.slice_off, M->sell.vals, M->sell.cols, x->d, y->d, static_cast< int64_t >( M->nrows ) );
 		} else {

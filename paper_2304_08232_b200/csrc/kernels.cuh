@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 namespace slabgpu {
+	struct Decomp;
 	namespace kern {
 
 		// ---- vector ops (operations.hpp:49-106)
@@ -50,13 +51,16 @@ namespace slabgpu {
 			unsigned int * iter_counter );
 
 		// ---- setup: 27-point stencil straight into SELL (problem.hpp:90-131), colour row lists
-		void stencil_widths( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos,
-			int64_t nslices, int32_t * widths );
-		void stencil_fill( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
+		void stencil_widths( cudaStream_t st, const Decomp & D, const int32_t * rows, int64_t npos, int64_t nslices,
+			int32_t * widths );
+		void stencil_fill( cudaStream_t st, const Decomp & D, const int32_t * rows, int64_t npos, int64_t nslices,
 			const int64_t * slice_off, double * vals, int32_t * cols );
-		// rows[pos0 + q] = natural index of the q-th member of parity class (px,py,pz), -1 beyond `size`
-		void color_rows( cudaStream_t st, int nx, int ny, int nz, int px, int py, int pz, int64_t pos0, int64_t size,
-			int64_t padded, int32_t * rows );
+		// rows[pos0 + q] = local index of the q-th owned member of global parity class `color`, -1 beyond `size`
+		void color_rows( cudaStream_t st, const Decomp & D, int color, int64_t pos0, int64_t size, int64_t padded,
+			int32_t * rows );
+		// halo pack: buf[dst[k]] = v[src[k]]
+		void halo_pack( cudaStream_t st, const int32_t * src, const int32_t * dst, int64_t count, const double * v,
+			double * buf );
 		// fine[c] = linear index of (2cx,2cy,2cz) (problem.hpp:189-195)
 		void injection_cols( cudaStream_t st, int nx, int ny, int nz, int32_t * fine );
 		// widths/cols/vals of a one-entry-per-row SELL from a column list

@@ -1,11 +1,13 @@
 // kernels_setup.cu — setup-time kernels: the 27-point stencil generated straight into SELL-32
-// (problem.hpp:90-131), colour row lists, the injection restriction (problem.hpp:174-201) and the
-// SELL -> CSR download path. None of these run inside a solve.
+// (problem.hpp:90-131) for the box a rank owns (the whole grid on one GPU), colour row lists, the
+// injection restriction (problem.hpp:174-201) and the SELL -> CSR download path. None of these
+// run inside a solve.
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
 
 #include "common.hpp"
+#include "decomp.hpp"
 
 namespace slabgpu {
 	namespace kern {
@@ -18,13 +20,17 @@ namespace slabgpu {
 				return static_cast< unsigned int >( ( count + block - 1 ) / block );
 			}
 
-			// ------------------------------------------------------------ setup kernels
-
-			__device__ __forceinline__ int span( int i, int n ) {
-				return ( i > 0 ? 1 : 0 ) + 1 + ( i + 1 < n ? 1 : 0 );
+			// owned row -> global coordinates
+			__device__ __forceinline__ void row_coords( const Decomp & D, int64_t i, int & X, int & Y, int & Z ) {
+				const int ix = static_cast< int >( i % D.l[ 0 ] );
+				const int iy = static_cast< int >( ( i / D.l[ 0 ] ) % D.l[ 1 ] );
+				const int iz = static_cast< int >( i / ( static_cast< int64_t >( D.l[ 0 ] ) * D.l[ 1 ] ) );
+				X = D.o[ 0 ] + ix;
+				Y = D.o[ 1 ] + iy;
+				Z = D.o[ 2 ] + iz;
 			}
 
-			__global__ void k_stencil_widths( int nx, int ny, int nz, const int32_t * __restrict__ rows, int64_t npos,
+			__global__ void k_stencil_widths( const Decomp D, const int32_t * __restrict__ rows, int64_t npos,
 				int64_t nslices, int32_t * __restrict__ widths ) {
 				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( ( pos >> 5 ) >= nslices ) {
@@ -34,10 +40,9 @@ namespace slabgpu {
 				if( pos < npos ) {
 					const int64_t i = rows ? rows[ pos ] : pos;
 					if( i >= 0 ) {
-						const int ix = static_cast< int >( i % nx );
-						const int iy = static_cast< int >( ( i / nx ) % ny );
-						const int iz = static_cast< int >( i / ( static_cast< int64_t >( nx ) * ny ) );
-						count = span( ix, nx ) * span( iy, ny ) * span( iz, nz );
+						int X, Y, Z;
+						row_coords( D, i, X, Y, Z );
+						count = span_1d( X, D.g[ 0 ] ) * span_1d( Y, D.g[ 1 ] ) * span_1d( Z, D.g[ 2 ] );
 					}
 				}
 				const int width = __reduce_max_sync( 0xffffffffu, count );
@@ -46,9 +51,10 @@ namespace slabgpu {
 				}
 			}
 
-			// problem.hpp:108-127: neighbours ascend lexicographically in (z,y,x), 26 on the
-			// diagonal and -1 off it; remaining slots of the slice are padding (col -1).
-			__global__ void k_stencil_fill( int nx, int ny, int nz, const int32_t * __restrict__ rows, int64_t npos,
+			// problem.hpp:108-127: neighbours ascend lexicographically in (z,y,x) of the GLOBAL grid,
+			// 26 on the diagonal and -1 off it; columns are local indices (owned or ghost);
+			// remaining slots of the slice are padding (col -1).
+			__global__ void k_stencil_fill( const Decomp D, const int32_t * __restrict__ rows, int64_t npos,
 				int64_t nslices, const int64_t * __restrict__ slice_off, double * __restrict__ vals,
 				int32_t * __restrict__ cols ) {
 				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -60,15 +66,14 @@ namespace slabgpu {
 				const int64_t end = slice_off[ s + 1 ];
 				const int64_t i = pos < npos ? ( rows ? rows[ pos ] : pos ) : -1;
 				if( i >= 0 ) {
-					const int ix = static_cast< int >( i % nx );
-					const int iy = static_cast< int >( ( i / nx ) % ny );
-					const int iz = static_cast< int >( i / ( static_cast< int64_t >( nx ) * ny ) );
-					for( int jz = iz > 0 ? iz - 1 : 0; jz < nz && jz <= iz + 1; ++jz ) {
-						for( int jy = iy > 0 ? iy - 1 : 0; jy < ny && jy <= iy + 1; ++jy ) {
-							for( int jx = ix > 0 ? ix - 1 : 0; jx < nx && jx <= ix + 1; ++jx ) {
-								const int64_t j = jx + static_cast< int64_t >( nx ) * ( jy + static_cast< int64_t >( ny ) * jz );
-								vals[ e ] = j == i ? 26.0 : -1.0;
-								cols[ e ] = static_cast< int32_t >( j );
+					int X, Y, Z;
+					row_coords( D, i, X, Y, Z );
+					for( int jz = Z > 0 ? Z - 1 : 0; jz < D.g[ 2 ] && jz <= Z + 1; ++jz ) {
+						for( int jy = Y > 0 ? Y - 1 : 0; jy < D.g[ 1 ] && jy <= Y + 1; ++jy ) {
+							for( int jx = X > 0 ? X - 1 : 0; jx < D.g[ 0 ] && jx <= X + 1; ++jx ) {
+								const bool diagonal = jx == X && jy == Y && jz == Z;
+								vals[ e ] = diagonal ? 26.0 : -1.0;
+								cols[ e ] = local_index( D, jx, jy, jz );
 								e += kSlice;
 							}
 						}
@@ -80,19 +85,24 @@ namespace slabgpu {
 				}
 			}
 
-			__global__ void k_color_rows( int nx, int ny, int px, int py, int pz, int sx, int sy, int64_t pos0, int64_t size,
-				int64_t padded, int32_t * __restrict__ rows ) {
+			// members of global parity class (cx,cy,cz) inside the owned box, ascending local index
+			__global__ void k_color_rows( const Decomp D, int cx, int cy, int cz, int64_t pos0, int64_t size, int64_t padded,
+				int32_t * __restrict__ rows ) {
 				const int64_t q = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( q >= padded ) {
 					return;
 				}
 				int32_t out = -1;
 				if( q < size ) {
-					const int cx = static_cast< int >( q % sx );
-					const int cy = static_cast< int >( ( q / sx ) % sy );
-					const int cz = static_cast< int >( q / ( static_cast< int64_t >( sx ) * sy ) );
-					out = static_cast< int32_t >( ( 2 * cx + px )
-						+ static_cast< int64_t >( nx ) * ( ( 2 * cy + py ) + static_cast< int64_t >( ny ) * ( 2 * cz + pz ) ) );
+					const int sx = count_parity( D.o[ 0 ], D.l[ 0 ], cx );
+					const int sy = count_parity( D.o[ 1 ], D.l[ 1 ], cy );
+					const int qx = static_cast< int >( q % sx );
+					const int qy = static_cast< int >( ( q / sx ) % sy );
+					const int qz = static_cast< int >( q / ( static_cast< int64_t >( sx ) * sy ) );
+					const int ix = first_parity( D.o[ 0 ], cx ) - D.o[ 0 ] + 2 * qx;
+					const int iy = first_parity( D.o[ 1 ], cy ) - D.o[ 1 ] + 2 * qy;
+					const int iz = first_parity( D.o[ 2 ], cz ) - D.o[ 2 ] + 2 * qz;
+					out = static_cast< int32_t >( ix + static_cast< int64_t >( D.l[ 0 ] ) * ( iy + static_cast< int64_t >( D.l[ 1 ] ) * iz ) );
 				}
 				rows[ pos0 + q ] = out;
 			}
@@ -151,37 +161,43 @@ namespace slabgpu {
 				}
 			}
 
+			// halo pack: buf[dst[k]] = v[src[k]]  (dst == nullptr: buf[k])
+			__global__ void k_halo_pack( const int32_t * __restrict__ src, const int32_t * __restrict__ dst, int64_t count,
+				const double * __restrict__ v, double * __restrict__ buf ) {
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( k < count ) {
+					buf[ dst != nullptr ? dst[ k ] : k ] = v[ src[ k ] ];
+				}
+			}
+
 		} // namespace
 
-		void stencil_widths( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
+		void stencil_widths( cudaStream_t st, const Decomp & D, const int32_t * rows, int64_t npos, int64_t nslices,
 			int32_t * widths ) {
 			if( nslices == 0 ) {
 				return;
 			}
-			k_stencil_widths<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( nx, ny, nz, rows, npos, nslices, widths );
+			k_stencil_widths<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( D, rows, npos, nslices, widths );
 			count_launch();
 		}
 
-		void stencil_fill( cudaStream_t st, int nx, int ny, int nz, const int32_t * rows, int64_t npos, int64_t nslices,
+		void stencil_fill( cudaStream_t st, const Decomp & D, const int32_t * rows, int64_t npos, int64_t nslices,
 			const int64_t * slice_off, double * vals, int32_t * cols ) {
 			if( nslices == 0 ) {
 				return;
 			}
-			k_stencil_fill<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( nx, ny, nz, rows, npos, nslices, slice_off,
-				vals, cols );
+			k_stencil_fill<<< blocks_for( nslices * kSlice ), kBlock, 0, st >>>( D, rows, npos, nslices, slice_off, vals,
+				cols );
 			count_launch();
 		}
 
-		void color_rows( cudaStream_t st, int nx, int ny, int nz, int px, int py, int pz, int64_t pos0, int64_t size,
-			int64_t padded, int32_t * rows ) {
-			(void) nz;
+		void color_rows( cudaStream_t st, const Decomp & D, int color, int64_t pos0, int64_t size, int64_t padded,
+			int32_t * rows ) {
 			if( padded == 0 ) {
 				return;
 			}
-			const int sx = ( nx + 1 - px ) / 2;
-			const int sy = ( ny + 1 - py ) / 2;
-			k_color_rows<<< blocks_for( padded ), kBlock, 0, st >>>( nx, ny, px, py, pz, sx > 0 ? sx : 1, sy > 0 ? sy : 1,
-				pos0, size, padded, rows );
+			k_color_rows<<< blocks_for( padded ), kBlock, 0, st >>>( D, color & 1, ( color >> 1 ) & 1, ( color >> 2 ) & 1, pos0,
+				size, padded, rows );
 			count_launch();
 		}
 
@@ -220,6 +236,15 @@ namespace slabgpu {
 			}
 			k_sell_to_csr<<< blocks_for( nrows ), kBlock, 0, st >>>( slice_off, vals, cols, nrows, row_off, out_cols,
 				out_vals );
+			count_launch();
+		}
+
+		void halo_pack( cudaStream_t st, const int32_t * src, const int32_t * dst, int64_t count, const double * v,
+			double * buf ) {
+			if( count == 0 ) {
+				return;
+			}
+			k_halo_pack<<< blocks_for( count ), kBlock, 0, st >>>( src, dst, count, v, buf );
 			count_launch();
 		}
 

@@ -14,6 +14,7 @@ slab_level_s::~slab_level_s() {
 	if( vcycle_exec ) {
 		cudaGraphExecDestroy( vcycle_exec );
 	}
+	slabgpu::halo_plan_destroy( plan );
 }
 
 namespace slabgpu {
@@ -22,15 +23,6 @@ namespace slabgpu {
 
 		int64_t round_up( int64_t v, int64_t m ) {
 			return ( v + m - 1 ) / m * m;
-		}
-
-		// sum over the points of one parity class along one axis of the 1D neighbour count
-		uint64_t span_sum( uint64_t n, uint64_t parity ) {
-			uint64_t total = 0;
-			for( uint64_t i = parity; i < n; i += 2 ) {
-				total += ( i > 0 ? 1 : 0 ) + 1 + ( i + 1 < n ? 1 : 0 );
-			}
-			return total;
 		}
 
 		void alloc_scratch( slab_level_s * L, uint64_t n_coarse ) {
@@ -52,28 +44,44 @@ namespace slabgpu {
 			L->dims[ 1 ] = ny;
 			L->dims[ 2 ] = nz;
 			L->is_stencil = true;
-			L->A.reset( mat_stencil27( ctx, nx, ny, nz ) );
+			// the box this rank owns (the whole grid on a single-process context); colours are the
+			// parity classes of the GLOBAL coordinates, so they agree with the single-process
+			// colouring even where a rank's offset is odd
+			const Decomp D = level_decomp( ctx, nx, ny, nz );
+			L->decomp = D;
+			L->A.reset( mat_stencil27_box( ctx, D ) );
 			L->n = L->A->nrows;
 			L->nnz = L->A->nnz;
+			if( ctx->dist != nullptr ) {
+				L->plan = halo_plan_create( ctx, D );
+				L->A->plan = L->plan;
+			}
 			L->num_colors = 8;
 			L->color_pos.assign( 9, 0 );
 			L->color_size.assign( 8, 0 );
 			L->color_nnz.assign( 8, 0 );
 			for( int k = 0; k < 8; ++k ) {
-				const uint64_t px = k & 1, py = ( k >> 1 ) & 1, pz = ( k >> 2 ) & 1;
-				const uint64_t sx = ( nx + 1 - px ) / 2, sy = ( ny + 1 - py ) / 2, sz = ( nz + 1 - pz ) / 2;
-				L->color_size[ k ] = sx * sy * sz;
-				L->color_nnz[ k ] = span_sum( nx, px ) * span_sum( ny, py ) * span_sum( nz, pz );
-				L->color_pos[ k + 1 ] = L->color_pos[ k ] + round_up( static_cast< int64_t >( L->color_size[ k ] ), kSlice );
+				const int c[ 3 ] = { k & 1, ( k >> 1 ) & 1, ( k >> 2 ) & 1 };
+				uint64_t size = 1, cnnz = 1;
+				for( int a = 0; a < 3; ++a ) {
+					size *= static_cast< uint64_t >( count_parity( D.o[ a ], D.l[ a ], c[ a ] ) );
+					uint64_t spans = 0;
+					for( int t = first_parity( D.o[ a ], c[ a ] ); t < D.o[ a ] + D.l[ a ]; t += 2 ) {
+						spans += static_cast< uint64_t >( span_1d( t, D.g[ a ] ) );
+					}
+					cnnz *= spans;
+				}
+				L->color_size[ k ] = size;
+				L->color_nnz[ k ] = cnnz;
+				L->color_pos[ k + 1 ] = L->color_pos[ k ] + round_up( static_cast< int64_t >( size ), kSlice );
 			}
 			const int64_t npos = L->color_pos[ 8 ];
 			SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< int64_t >( npos, 1 ) * sizeof( int32_t ) ) );
 			for( int k = 0; k < 8; ++k ) {
-				kern::color_rows( ctx->stream, static_cast< int >( nx ), static_cast< int >( ny ), static_cast< int >( nz ),
-					k & 1, ( k >> 1 ) & 1, ( k >> 2 ) & 1, L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ),
+				kern::color_rows( ctx->stream, D, k, L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ),
 					L->color_pos[ k + 1 ] - L->color_pos[ k ], L->d_rows );
 			}
-			L->colorA = sell_stencil27( ctx, nx, ny, nz, L->d_rows, npos );
+			L->colorA = sell_stencil27( ctx, D, L->d_rows, npos );
 			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
 			uint64_t n_coarse = 0;
 			if( with_restriction ) {
@@ -232,24 +240,28 @@ namespace slabgpu {
 			}
 		}
 
-		void color_step_enqueue( slab_level_s * L, uint64_t k, double * z, const double * r ) {
+		// One colour step. Invariant on distributed levels: the ghost copies of z are current on
+		// entry; the step then sends the just-updated boundary values of colour k to the neighbours
+		// (only that colour moved), which restores the invariant for the next step.
+		void color_step_enqueue( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r ) {
 			kern::gs_color_step( L->ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
-				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z, r );
+				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z->d, r->d );
+			halo_exchange( L, z, static_cast< int >( k ) );
 		}
 
-		void forward_enqueue( slab_level_s * L, double * z, const double * r ) { // smoother.hpp:80-82
+		void forward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:80-82
 			for( uint64_t k = 0; k < L->num_colors; ++k ) {
 				color_step_enqueue( L, k, z, r );
 			}
 		}
 
-		void backward_enqueue( slab_level_s * L, double * z, const double * r ) { // smoother.hpp:95-97
+		void backward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:95-97
 			for( uint64_t k = L->num_colors; k > 0; --k ) {
 				color_step_enqueue( L, k - 1, z, r );
 			}
 		}
 
-		void symmetric_enqueue( slab_level_s * L, double * z, const double * r, uint64_t sweeps ) { // smoother.hpp:108-111
+		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) { // smoother.hpp:108-111
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
 				forward_enqueue( L, z, r );
 				backward_enqueue( L, z, r );
@@ -262,19 +274,22 @@ namespace slabgpu {
 		if( k >= L->num_colors ) {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "rbgs_color_step: colour index out of range" );
 		}
-		color_step_enqueue( L, k, z->d, r->d );
+		halo_exchange( L, z, -1 ); // z is the caller's: its ghost copies may be stale
+		color_step_enqueue( L, k, z, r );
 		L->stats.nnz_visited += L->color_nnz[ k ]; // smoother.hpp:71
 	}
 
 	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
 		check_smoother_args( L, z, r );
-		forward_enqueue( L, z->d, r->d );
+		halo_exchange( L, z, -1 );
+		forward_enqueue( L, z, r );
 		L->stats.nnz_visited += L->nnz;
 	}
 
 	void rbgs_backward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
 		check_smoother_args( L, z, r );
-		backward_enqueue( L, z->d, r->d );
+		halo_exchange( L, z, -1 );
+		backward_enqueue( L, z, r );
 		L->stats.nnz_visited += L->nnz;
 	}
 
@@ -283,7 +298,8 @@ namespace slabgpu {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
 		}
 		check_smoother_args( L, z, r );
-		symmetric_enqueue( L, z->d, r->d, sweeps );
+		halo_exchange( L, z, -1 );
+		symmetric_enqueue( L, z, r, sweeps );
 		L->stats.nnz_visited += 2 * sweeps * L->nnz;
 	}
 
@@ -329,7 +345,7 @@ namespace slabgpu {
 	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
 	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats ) {
 		slab_ctx_s * ctx = L->ctx;
-		symmetric_enqueue( L, z->d, r->d, sweeps );
+		symmetric_enqueue( L, z, r, sweeps );
 		if( !L->coarser ) {
 			if( count_stats ) {
 				L->stats.nnz_visited += 2 * sweeps * L->nnz;
@@ -352,7 +368,7 @@ namespace slabgpu {
 			op_mxv( L->f.get(), nullptr, L->R.get(), L->z_c.get(), SLAB_DESC_TRANSPOSE );
 			op_waxpby( z, 1.0, z, 1.0, L->f.get() );
 		}
-		symmetric_enqueue( L, z->d, r->d, sweeps );
+		symmetric_enqueue( L, z, r, sweeps );
 		if( count_stats ) {
 			L->stats.nnz_visited += 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz;
 		}
@@ -367,6 +383,7 @@ namespace slabgpu {
 		}
 		slab_ctx_s * ctx = L->ctx;
 		if( !ctx->use_graphs ) {
+			halo_exchange( L, z, -1 ); // the caller's z: ghost copies may be stale
 			mg_vcycle_enqueue( L, z, r, sweeps, true );
 			return;
 		}
@@ -386,6 +403,7 @@ namespace slabgpu {
 			const uint64_t launches_before = g_launch_count;
 			SLAB_CUDA( cudaStreamBeginCapture( ctx->stream, cudaStreamCaptureModeThreadLocal ) );
 			try {
+				halo_exchange( L, z, -1 );
 				mg_vcycle_enqueue( L, z, r, sweeps, false );
 			} catch( ... ) {
 				cudaStreamEndCapture( ctx->stream, &graph );
