@@ -85,9 +85,16 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_stream_variant = static_cast< int >( value );
 		} else if( k == "pdl" ) {
 			g_use_pdl = value ? 1 : 0;
+		} else if( k == "persist_rows" ) {
+			g_persist_rows = value;
+		} else if( k == "persist_debug" ) {
+			g_persist_debug = static_cast< int >( value );
+		} else if( k == "persist_blocks_per_sm" ) {
+			g_persist_blocks_per_sm = static_cast< int >( value );
 		} else {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "slab_set_tuning: unknown key " + k );
 		}
+		++g_tuning_epoch;
 	} );
 }
 
@@ -127,6 +134,12 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		if( const char * v = std::getenv( "SLAB_STREAM_VARIANT" ) ) {
 			g_stream_variant = std::atoi( v );
 		}
+		if( const char * v = std::getenv( "SLAB_PERSIST_ROWS" ) ) {
+			g_persist_rows = std::atoll( v );
+		}
+		if( const char * v = std::getenv( "SLAB_PERSIST_BLOCKS_PER_SM" ) ) {
+			g_persist_blocks_per_sm = std::atoi( v );
+		}
 		std::unique_ptr< slab_ctx_s > ctx( new slab_ctx_s );
 		ctx->device = device;
 		ctx->sm_count = prop.multiProcessorCount;
@@ -160,6 +173,7 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		cudaFree( ctx->d_scalars );
 		cudaFree( ctx->d_partials );
 		cudaFree( ctx->d_counter );
+		cudaFree( ctx->d_barrier );
 		if( ctx->h_pinned ) cudaFreeHost( ctx->h_pinned );
 		cudaEventDestroy( ctx->timer_start );
 		cudaEventDestroy( ctx->timer_stop );

@@ -134,15 +134,13 @@ namespace slabgpu {
 
 		// iteration graph, cached per (x, config)
 		const bool graphs = ctx->use_graphs != 0;
+		if( cfg->use_preconditioner && limit > 0 ) {
+			mg_vcycle_prepare( H, ws->z.get(), ws->r.get(), cfg->sweeps ); // before any capture
+		}
 		if( graphs && limit > 0 ) {
-			if( !ctx->fused_transfers && cfg->use_preconditioner ) {
-				for( slab_level_s * at = H; at && at->R; at = at->coarser.get() ) {
-					mat_transposed( at->R.get() );
-				}
-			}
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
-				|| ws->key_fused != ctx->fused_transfers;
+				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch;
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -174,6 +172,7 @@ namespace slabgpu {
 				ws->key_precond = cfg->use_preconditioner;
 				ws->key_dot = ctx->dot_mode;
 				ws->key_fused = ctx->fused_transfers;
+				ws->key_epoch = g_tuning_epoch;
 			}
 		}
 

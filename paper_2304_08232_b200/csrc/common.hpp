@@ -52,6 +52,10 @@ namespace slabgpu {
 		SLAB_CUDA( cudaStreamSynchronize( stream ) );
 	}
 
+	extern uint64_t g_tuning_epoch;  // bumped by every slab_set_tuning: cached graphs are keyed by it
+	extern int64_t g_persist_rows;   // levels whose largest colour has fewer rows run inside the persistent kernel (0 = off)
+	extern int g_persist_blocks_per_sm;
+	extern int g_persist_debug;
 	extern int64_t g_stream_rows;
 	extern int g_stream_variant;
 	extern uint64_t g_launch_count;
@@ -99,6 +103,8 @@ struct slab_ctx_s {
 	double * d_partials = nullptr;  // reduction scratch
 	uint64_t partials_cap = 0;
 	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
+	unsigned int * d_barrier = nullptr; // grid barrier of the persistent V-cycle kernel: {arrivals, generation}
+	int persist_grid = 0;               // blocks of the persistent kernel (0 = not yet sized)
 	double * h_pinned = nullptr;    // pinned staging for scalar read-back
 	uint64_t h_pinned_cap = 0;
 	cudaEvent_t timer_start = nullptr, timer_stop = nullptr; // slab_ctx_timer_* (caller-owned interval)
@@ -168,7 +174,15 @@ struct slab_level_s {
 	double * vcycle_r = nullptr;
 	uint64_t vcycle_sweeps = 0;
 	int vcycle_fused = -1;
+	uint64_t vcycle_epoch = ~uint64_t( 0 );
 	uint64_t vcycle_launches = 0;
+	// persistent sub-V-cycle rooted at this level: device phase list, keyed by the vectors it addresses
+	void * d_phases = nullptr;
+	int nphases = 0;
+	int phases_grid = 1;
+	double * phases_z = nullptr;
+	double * phases_r = nullptr;
+	uint64_t phases_sweeps = 0;
 	// CG workspace of the hierarchy head: r, z, p, q, device history, iteration graph
 	std::unique_ptr< slabgpu::CgWorkspace > cg;
 	~slab_level_s();
@@ -187,6 +201,7 @@ namespace slabgpu {
 		double * key_x = nullptr;
 		uint64_t key_sweeps = 0;
 		int key_precond = -1, key_dot = -1, key_fused = -1;
+		uint64_t key_epoch = ~uint64_t( 0 );
 		uint64_t iter_launches = 0;
 		~CgWorkspace();
 	};
@@ -235,6 +250,9 @@ namespace slabgpu {
 	void refine_and_add( slab_level_s * L, slab_vec_s * z, slab_vec_s * z_c );
 	void mg_vcycle( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
 	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats );
+	// everything mg_vcycle_enqueue needs that may allocate or copy (phase lists of the persistent kernel,
+	// lazily built transposes): must run before stream capture begins
+	void mg_vcycle_prepare( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
 
 	// ---- ops (kernels.cu)
 	void op_set_all( slab_vec_s * v, double value );

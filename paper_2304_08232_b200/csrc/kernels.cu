@@ -25,6 +25,11 @@ namespace slabgpu {
 
 	uint64_t g_launch_count = 0;
 	int g_use_pdl = 1;
+	uint64_t g_tuning_epoch = 0;
+	// levels whose largest colour has fewer rows than this run inside the persistent V-cycle kernel
+	int64_t g_persist_rows = 100000;
+	int g_persist_blocks_per_sm = 1;
+	int g_persist_debug = 0; // timing experiments only: 1 = barriers without work, 2 = work without grid barriers
 	// launches with at least this many rows use the streaming kernels, smaller ones the preload
 	// kernels (measured cross-over on B200: ~1e5 rows, a third of a full wave of 148 SMs x 2048 threads)
 	int64_t g_stream_rows = 100000;
@@ -400,7 +405,9 @@ namespace slabgpu {
 			// Batched streaming row sum: B (column, value) pairs are loaded together, then their B
 			// gathers, then the B-long ordered add chain; the next batch's matrix loads are issued
 			// before the chain of the current one runs (software pipelining by hand).
-			template< int B, bool WANT_DIAG >
+			// COHERENT: gather x through L2 only (ld.global.cg) — needed inside the persistent V-cycle
+			// kernel, where other SMs update x between grid barriers and L1 would serve stale lines.
+			template< int B, bool WANT_DIAG, bool COHERENT = false >
 			__device__ __forceinline__ double row_sum_batched( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, int64_t pos, const double * x,
 				int32_t diag_row, double & diag ) {
@@ -422,7 +429,7 @@ namespace slabgpu {
 					double xv[ B ];
 					#pragma unroll
 					for( int j = 0; j < B; ++j ) {
-						xv[ j ] = x[ c[ j ] < 0 ? 0 : c[ j ] ];
+						xv[ j ] = COHERENT ? __ldcg( x + ( c[ j ] < 0 ? 0 : c[ j ] ) ) : x[ c[ j ] < 0 ? 0 : c[ j ] ];
 					}
 					int32_t cc[ B ];
 					double vv[ B ];
@@ -485,6 +492,173 @@ namespace slabgpu {
 				}
 				double unused = 0.0;
 				y[ row ] = row_sum_batched< B, false >( slice_off, vals, cols, row, x, -1, unused );
+			}
+
+			// ---- persistent sub-V-cycle (coarse levels): phases separated by a grid barrier
+
+			// sense-reversing grid barrier; bar[0] = arrival counter, bar[1] = generation. All blocks are
+			// co-resident (cooperative launch). Writes before the barrier are visible device-wide after
+			// it (thread 0 fences on both sides, the block barriers extend that to the whole block).
+			__device__ __forceinline__ unsigned int atom_add_release( unsigned int * p, unsigned int v ) {
+				unsigned int old;
+				asm volatile( "atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"( old ) : "l"( p ), "r"( v ) : "memory" );
+				return old;
+			}
+			__device__ __forceinline__ unsigned int load_acquire( const unsigned int * p ) {
+				unsigned int v;
+				asm volatile( "ld.acquire.gpu.global.u32 %0, [%1];" : "=r"( v ) : "l"( p ) : "memory" );
+				return v;
+			}
+			__device__ __forceinline__ void store_release( unsigned int * p, unsigned int v ) {
+				asm volatile( "st.release.gpu.global.u32 [%0], %1;" ::"l"( p ), "r"( v ) : "memory" );
+			}
+
+			// Split grid barrier. `generation` is thread 0's running copy of bar[32] (barriers are strictly
+			// sequential, so it never has to be re-read). arrive: one release-atomic by thread 0, cumulative
+			// over the block's writes through the preceding block barrier. Between arrive and wait the block
+			// may issue loads of IMMUTABLE data (the next phase's matrix rows) — issued after the release they
+			// are not ordered before it and overlap the barrier latency. wait: acquire poll plus a gpu-scope
+			// fence, which invalidates the SM's L1 so that later plain loads see the other SMs' writes.
+			__device__ __forceinline__ void grid_arrive( unsigned int * bar, unsigned int nblocks, unsigned int & generation,
+				bool & last ) {
+				__syncthreads();
+				if( threadIdx.x == 0 ) {
+					last = atom_add_release( bar, 1u ) == nblocks - 1;
+					generation += 1u;
+				}
+			}
+			__device__ __forceinline__ void grid_wait( unsigned int * bar, unsigned int generation, bool last ) {
+				if( threadIdx.x == 0 ) {
+					unsigned int * gen = bar + 32; // a different 128 B line than the arrival counter
+					if( last ) {
+						bar[ 0 ] = 0u;
+						store_release( gen, generation );
+					} else {
+						while( load_acquire( gen ) != generation ) {
+							__nanosleep( 20 );
+						}
+					}
+					__threadfence();
+				}
+				__syncthreads();
+			}
+
+			constexpr int kMaxPhases = 192; // phase descriptors staged in shared memory
+
+			// One colour-step row of the persistent kernel. `rc` holds the row's matrix entries (loaded
+			// before the preceding grid barrier); all 27 gathers go out together. Plain (L1-cached)
+			// loads are correct here: the grid barrier ends with a gpu-scope fence by thread 0 followed by
+			// a block barrier, which orders every later load of the block after the other SMs' released
+			// writes (the fence invalidates the SM's L1), exactly like cooperative-groups grid.sync().
+			//  PROLONG (flags & 1): z[i] <- 1*z[i] + 1*(0 + 1*src[k]) first (multigrid.hpp:71-81 at the injected
+			//    row); the updated value also replaces the stale diagonal gather.
+			//  RESID (flags & 2): after the update, r_c[k] = 0 + 1*(1*r[i] + (-1)*(A z)[i]) with the NEW z[i] on
+			//    the diagonal (multigrid.hpp:100-104): all other colours are final in the last backward step.
+			__device__ __forceinline__ void persistent_row( const VcyclePhase & ph, int64_t k, int32_t i, const RowChunk & rc,
+				int width ) {
+				double xv[ kChunk ];
+				#pragma unroll
+				for( int j = 0; j < kChunk; ++j ) {
+					xv[ j ] = j < width ? ph.z[ rc.c[ j ] < 0 ? 0 : rc.c[ j ] ] : 0.0;
+				}
+				double zi = ph.z[ i ];
+				const double ri = ph.r[ i ];
+				if( ph.flags & 1 ) {
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, ph.src[ k ] ) );
+					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+				}
+				double s = 0.0, d = 0.0;
+				#pragma unroll
+				for( int j = 0; j < kChunk; ++j ) {
+					if( j < width ) {
+						const bool diagonal = rc.c[ j ] == i;
+						const double xj = ( ( ph.flags & 1 ) && diagonal ) ? zi : xv[ j ];
+						const double sum = __dadd_rn( s, __dmul_rn( rc.v[ j ], xj ) );
+						s = rc.c[ j ] < 0 ? s : sum;
+						d = diagonal ? rc.v[ j ] : d;
+					}
+				}
+				const double znew = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+				ph.z[ i ] = znew;
+				if( ph.flags & 2 ) {
+					double az = 0.0;
+					#pragma unroll
+					for( int j = 0; j < kChunk; ++j ) {
+						if( j < width ) {
+							const double xj = rc.c[ j ] == i ? znew : xv[ j ];
+							const double sum = __dadd_rn( az, __dmul_rn( rc.v[ j ], xj ) );
+							az = rc.c[ j ] < 0 ? az : sum;
+						}
+					}
+					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
+					ph.out[ k ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+				}
+			}
+
+			__device__ __forceinline__ void persistent_load( const VcyclePhase & ph, int64_t k, int32_t & i, RowChunk & rc,
+				int & width ) {
+				const int64_t pos = ph.pos_begin + k;
+				i = ph.rows[ pos ];
+				const int64_t s = pos >> 5;
+				const int64_t b = ph.slice_off[ s ];
+				width = static_cast< int >( ( ph.slice_off[ s + 1 ] - b ) >> 5 );
+				chunk_load( ph.vals, ph.cols, b + ( pos & 31 ), width, rc );
+			}
+
+			// One block per SM, all co-resident (cooperative launch). Every phase is one colour step of one
+			// level (smoother.hpp:60-72) with the grid transfers fused into the neighbouring colour-0 steps.
+			// A thread owns row k = its global index of every phase; the matrix entries of its NEXT row
+			// are fetched before the grid barrier, so after the barrier only the z gathers (L2 latency), the
+			// ordered add chain and one store separate two barriers.
+			__global__ void __launch_bounds__( kBlock, 1 ) k_vcycle_persistent( const VcyclePhase * __restrict__ phases,
+				int nphases, unsigned int * bar, int debug ) {
+				__shared__ VcyclePhase sph[ kMaxPhases ];
+				for( int t = threadIdx.x; t < nphases * static_cast< int >( sizeof( VcyclePhase ) / 8 ); t += blockDim.x ) {
+					reinterpret_cast< uint64_t * >( sph )[ t ] = reinterpret_cast< const uint64_t * >( phases )[ t ];
+				}
+				__syncthreads();
+				const int64_t gtid = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const int64_t gsize = static_cast< int64_t >( gridDim.x ) * blockDim.x;
+				RowChunk rc;
+				int32_t row = -1;
+				int width = 0;
+				unsigned int generation = threadIdx.x == 0 ? *reinterpret_cast< volatile unsigned int * >( bar + 32 ) : 0u;
+				if( gtid < sph[ 0 ].count ) {
+					persistent_load( sph[ 0 ], gtid, row, rc, width );
+				}
+				for( int p = 0; p < nphases; ++p ) {
+					const VcyclePhase & ph = sph[ p ];
+					if( gtid < ph.count && row >= 0 && debug != 1 ) {
+						persistent_row( ph, gtid, row, rc, width );
+					}
+					for( int64_t k = gtid + gsize; k < ph.count; k += gsize ) { // phases larger than the grid
+						RowChunk extra;
+						int32_t i;
+						int w;
+						persistent_load( ph, k, i, extra, w );
+						if( i >= 0 ) {
+							persistent_row( ph, k, i, extra, w );
+						}
+					}
+					for( int64_t k = gtid; k < ph.zero_count; k += gsize ) { // set_all(z_c, 0), multigrid.hpp:104
+						ph.zero[ k ] = 0.0;
+					}
+					if( p + 1 < nphases ) {
+						bool last = false;
+						if( debug != 2 ) {
+							grid_arrive( bar, gridDim.x, generation, last );
+						}
+						row = -1;
+						if( gtid < sph[ p + 1 ].count ) {
+							persistent_load( sph[ p + 1 ], gtid, row, rc, width ); // immutable data, overlaps the barrier
+						}
+						if( debug != 2 ) {
+							grid_wait( bar, generation, last );
+						} else {
+							__syncthreads();
+						}
+					}
+				}
 			}
 
 			// ---- streaming forms (many-wave launches on the fine level); same arithmetic, same order
@@ -740,6 +914,35 @@ namespace slabgpu {
 				return;
 			}
 			launch( k_prolong_add, blocks_for( n_coarse ), kBlock, st, rows, n_coarse, z, z_c );
+		}
+
+		int vcycle_persistent_blocks( int sm_count, int blocks_per_sm ) {
+			int resident = 0;
+			SLAB_CUDA( cudaOccupancyMaxActiveBlocksPerMultiprocessor( &resident, k_vcycle_persistent, kBlock, 0 ) );
+			if( resident < 1 ) {
+				fail( SLAB_ERR_CUDA, "persistent V-cycle kernel cannot be resident" );
+			}
+			const int per_sm = blocks_per_sm < resident ? blocks_per_sm : resident;
+			return sm_count * ( per_sm < 1 ? 1 : per_sm );
+		}
+
+		void vcycle_persistent( cudaStream_t st, const VcyclePhase * d_phases, int nphases, unsigned int * d_barrier,
+			int grid_blocks ) {
+			if( nphases == 0 ) {
+				return;
+			}
+			cudaLaunchConfig_t cfg{};
+			cfg.gridDim = dim3( static_cast< unsigned int >( grid_blocks ), 1, 1 );
+			cfg.blockDim = dim3( kBlock, 1, 1 );
+			cfg.dynamicSmemBytes = 0;
+			cfg.stream = st;
+			cudaLaunchAttribute attr[ 1 ];
+			attr[ 0 ].id = cudaLaunchAttributeCooperative; // all blocks co-resident: the grid barrier is safe
+			attr[ 0 ].val.cooperative = 1;
+			cfg.attrs = attr;
+			cfg.numAttrs = 1;
+			SLAB_CUDA( cudaLaunchKernelEx( &cfg, k_vcycle_persistent, d_phases, nphases, d_barrier, g_persist_debug ) );
+			count_launch();
 		}
 
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,

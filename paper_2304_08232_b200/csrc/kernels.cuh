@@ -39,6 +39,29 @@ namespace slabgpu {
 		// z[i] = 1*z[i] + 1*(0 + 1*z_c[p]) at the injected rows
 		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c );
 
+		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
+		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a
+		// kernel launch (coarse levels are launch-latency-bound). Same arithmetic, same order.
+		struct VcyclePhase { // one colour step; 8-byte fields only (staged into shared memory word by word)
+			int64_t flags; // bit 0: prolongation fused in front (src), bit 1: residual+restriction fused behind (out)
+			const int64_t * slice_off;
+			const double * vals;
+			const int32_t * cols;
+			const int32_t * rows;
+			int64_t pos_begin;
+			int64_t count;
+			double * z;
+			const double * r;
+			const double * src; // flags&1: the coarse correction z_c, indexed by coarse row
+			double * out;       // flags&2: r_c
+			double * zero;      // flags&2: z_c, zeroed for the coarser level's start (multigrid.hpp:104)
+			int64_t zero_count;
+		};
+		constexpr int kVcycleMaxPhases = 192;
+		int vcycle_persistent_blocks( int sm_count, int blocks_per_sm );
+		void vcycle_persistent( cudaStream_t st, const VcyclePhase * d_phases, int nphases, unsigned int * d_barrier,
+			int grid_blocks );
+
 		// ---- CG vector updates with device-resident scalars (cg.hpp:116-132)
 		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,

@@ -15,6 +15,9 @@ slab_level_s::~slab_level_s() {
 		cudaGraphExecDestroy( vcycle_exec );
 	}
 	slabgpu::halo_plan_destroy( plan );
+	if( d_phases ) {
+		cudaFree( d_phases );
+	}
 }
 
 namespace slabgpu {
@@ -342,9 +345,163 @@ namespace slabgpu {
 		}
 	} // namespace
 
+	namespace {
+
+		// A level runs inside the persistent kernel when its colour steps are latency-bound (few rows),
+		// the fused transfers are on, and no halo exchange sits between its phases.
+		uint64_t persistent_phase_count( const slab_level_s * L, uint64_t sweeps );
+
+		bool use_persistent( const slab_level_s * L, uint64_t sweeps ) {
+			if( g_persist_rows <= 0 || !L->ctx->fused_transfers || L->num_colors == 0 ) {
+				return false;
+			}
+			if( L->plan != nullptr && L->decomp.n_ghost > 0 ) {
+				return false;
+			}
+			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
+				if( at->plan != nullptr && at->decomp.n_ghost > 0 ) {
+					return false;
+				}
+			}
+			if( !L->is_stencil ) {
+				return false; // the fused transfers rely on "colour 0 == injected rows" and rows of <= 27 entries
+			}
+			uint64_t largest = 0;
+			for( const uint64_t size : L->color_size ) {
+				largest = std::max( largest, size );
+			}
+			return static_cast< int64_t >( largest ) < g_persist_rows
+				&& persistent_phase_count( L, sweeps ) <= static_cast< uint64_t >( kern::kVcycleMaxPhases );
+		}
+
+		uint64_t persistent_phase_count( const slab_level_s * L, uint64_t sweeps ) {
+			uint64_t count = 0;
+			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
+				count += ( at->coarser ? 2 : 1 ) * 2 * sweeps * at->num_colors;
+			}
+			return count;
+		}
+
+		// multigrid.hpp:87-116 unrolled into the phase list of the sub-hierarchy rooted at L
+		void build_phases( slab_level_s * L, double * z, const double * r, uint64_t sweeps,
+			std::vector< kern::VcyclePhase > & out ) {
+			// On a stencil level the injected rows are exactly colour 0, in coarse-index order
+			// (position p of the colour-0 block <-> coarse row p). So the residual+restriction rides on
+			// the LAST colour step of the pre-smoother (backward, colour 0: every other colour is final
+			// by then) and the prolongation+update on the FIRST colour step of the post-smoother
+			// (forward, colour 0, which reads no other colour-0 value).
+			const auto color_step = [ & ]( uint64_t k, int64_t flags ) {
+				kern::VcyclePhase ph{};
+				ph.flags = flags;
+				ph.slice_off = L->colorA.slice_off;
+				ph.vals = L->colorA.vals;
+				ph.cols = L->colorA.cols;
+				ph.rows = L->d_rows;
+				ph.pos_begin = L->color_pos[ k ];
+				ph.count = static_cast< int64_t >( L->color_size[ k ] );
+				ph.z = z;
+				ph.r = r;
+				if( flags & 1 ) {
+					ph.src = L->z_c->d;
+				}
+				if( flags & 2 ) {
+					ph.out = L->r_c->d;
+					ph.zero = L->z_c->d;
+					ph.zero_count = static_cast< int64_t >( L->z_c->n_alloc );
+				}
+				out.push_back( ph );
+			};
+			const bool transfers = L->coarser != nullptr;
+			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) { // pre-smooth, multigrid.hpp:94
+				for( uint64_t k = 0; k < L->num_colors; ++k ) {
+					color_step( k, 0 );
+				}
+				for( uint64_t k = L->num_colors; k > 0; --k ) {
+					color_step( k - 1, transfers && sweep + 1 == sweeps && k == 1 ? 2 : 0 );
+				}
+			}
+			if( !transfers ) {
+				return;
+			}
+			build_phases( L->coarser.get(), L->z_c->d, L->r_c->d, sweeps, out );
+			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) { // post-smooth, multigrid.hpp:111
+				for( uint64_t k = 0; k < L->num_colors; ++k ) {
+					color_step( k, sweep == 0 && k == 0 ? 1 : 0 );
+				}
+				for( uint64_t k = L->num_colors; k > 0; --k ) {
+					color_step( k - 1, 0 );
+				}
+			}
+		}
+
+		void prepare_persistent( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
+			slab_ctx_s * ctx = L->ctx;
+			if( ctx->d_barrier == nullptr ) {
+				SLAB_CUDA( cudaMalloc( &ctx->d_barrier, 64 * sizeof( unsigned int ) ) );
+				const unsigned int zeros[ 64 ] = { 0u };
+				upload_sync( ctx->stream, ctx->d_barrier, zeros, sizeof( zeros ) );
+			}
+			if( ctx->persist_grid == 0 ) {
+				ctx->persist_grid = kern::vcycle_persistent_blocks( ctx->sm_count, g_persist_blocks_per_sm );
+			}
+			if( L->d_phases != nullptr && L->phases_z == z->d && L->phases_r == r->d && L->phases_sweeps == sweeps ) {
+				return;
+			}
+			std::vector< kern::VcyclePhase > phases;
+			build_phases( L, z->d, r->d, sweeps, phases );
+			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) ); // nobody may still be reading the old list
+			if( L->d_phases != nullptr ) {
+				cudaFree( L->d_phases );
+				L->d_phases = nullptr;
+			}
+			SLAB_CUDA( cudaMalloc( &L->d_phases, std::max< size_t >( phases.size(), 1 ) * sizeof( kern::VcyclePhase ) ) );
+			upload_sync( ctx->stream, L->d_phases, phases.data(), phases.size() * sizeof( kern::VcyclePhase ) );
+			L->nphases = static_cast< int >( phases.size() );
+			// as few blocks as the widest phase needs (one row per thread): the grid barrier gets cheaper
+			// with every block that does not take part
+			int64_t widest = 1;
+			for( const kern::VcyclePhase & ph : phases ) {
+				widest = std::max( widest, ph.count );
+			}
+			L->phases_grid = static_cast< int >( std::min< int64_t >( ctx->persist_grid, ( widest + 255 ) / 256 ) );
+			L->phases_z = z->d;
+			L->phases_r = r->d;
+			L->phases_sweeps = sweeps;
+		}
+
+	} // namespace
+
+	void mg_vcycle_prepare( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
+		slab_ctx_s * ctx = L->ctx;
+		if( !ctx->fused_transfers ) {
+			for( slab_level_s * at = L; at && at->R; at = at->coarser.get() ) {
+				mat_transposed( at->R.get() ); // built lazily; allocation is illegal during capture
+			}
+		}
+		for( slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
+			if( use_persistent( at, sweeps ) ) {
+				prepare_persistent( at, z, r, sweeps );
+				return;
+			}
+			z = at->z_c.get();
+			r = at->r_c.get();
+		}
+	}
+
 	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
 	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats ) {
 		slab_ctx_s * ctx = L->ctx;
+		if( use_persistent( L, sweeps ) ) {
+			if( L->d_phases == nullptr || L->phases_z != z->d || L->phases_r != r->d || L->phases_sweeps != sweeps ) {
+				fail( SLAB_ERR_INTERNAL, "persistent V-cycle used without mg_vcycle_prepare" );
+			}
+			kern::vcycle_persistent( ctx->stream, static_cast< const kern::VcyclePhase * >( L->d_phases ), L->nphases,
+				ctx->d_barrier, L->phases_grid );
+			if( count_stats ) {
+				vcycle_stats( L, sweeps );
+			}
+			return;
+		}
 		symmetric_enqueue( L, z, r, sweeps );
 		if( !L->coarser ) {
 			if( count_stats ) {
@@ -382,19 +539,14 @@ namespace slabgpu {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
 		}
 		slab_ctx_s * ctx = L->ctx;
+		mg_vcycle_prepare( L, z, r, sweeps ); // allocations and uploads happen before any capture
 		if( !ctx->use_graphs ) {
 			halo_exchange( L, z, -1 ); // the caller's z: ghost copies may be stale
 			mg_vcycle_enqueue( L, z, r, sweeps, true );
 			return;
 		}
-		// make sure lazily built transposes exist before capturing (they allocate)
-		if( !ctx->fused_transfers ) {
-			for( slab_level_s * at = L; at && at->R; at = at->coarser.get() ) {
-				mat_transposed( at->R.get() );
-			}
-		}
 		if( L->vcycle_exec == nullptr || L->vcycle_z != z->d || L->vcycle_r != r->d || L->vcycle_sweeps != sweeps
-			|| L->vcycle_fused != ctx->fused_transfers ) {
+			|| L->vcycle_fused != ctx->fused_transfers || L->vcycle_epoch != g_tuning_epoch ) {
 			if( L->vcycle_exec ) {
 				cudaGraphExecDestroy( L->vcycle_exec );
 				L->vcycle_exec = nullptr;
@@ -422,6 +574,7 @@ namespace slabgpu {
 			L->vcycle_r = r->d;
 			L->vcycle_sweeps = sweeps;
 			L->vcycle_fused = ctx->fused_transfers;
+			L->vcycle_epoch = g_tuning_epoch;
 		}
 		SLAB_CUDA( cudaGraphLaunch( L->vcycle_exec, ctx->stream ) );
 		count_launch( L->vcycle_launches );
