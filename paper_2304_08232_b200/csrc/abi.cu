@@ -98,6 +98,18 @@ int slab_set_tuning( const char * key, int64_t value ) {
 	} );
 }
 
+int slab_debug_read_barrier_words( slab_ctx_t ctx, long long * out6 ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_debug_read_barrier_words" );
+		need( out6, "slab_debug_read_barrier_words" );
+		if( ctx->d_barrier == nullptr ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "no persistent kernel has run on this context" );
+		}
+		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+		SLAB_CUDA( cudaMemcpy( out6, ctx->d_barrier + 40, 6 * sizeof( long long ), cudaMemcpyDeviceToHost ) );
+	} );
+}
+
 uint64_t slab_launch_count( void ) {
 	return g_launch_count;
 }

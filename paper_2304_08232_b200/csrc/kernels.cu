@@ -26,13 +26,16 @@ namespace slabgpu {
 	uint64_t g_launch_count = 0;
 	int g_use_pdl = 1;
 	uint64_t g_tuning_epoch = 0;
-	// levels whose largest colour has fewer rows than this run inside the persistent V-cycle kernel
-	int64_t g_persist_rows = 100000;
+	// levels whose largest colour has fewer rows than this run inside the persistent V-cycle kernel.
+	// OFF by default: measured on B200 (tools/persistent_probe.py) a phase costs 3.1-4.2 us (release
+	// atomic ~0.9 us + acquire poll/fence ~1.2 us + the row's own load->gather->add chain ~1.2 us), while
+	// the same colour step as a programmatically-dependent launch inside the CUDA graph costs 1.8-2.5 us.
+	int64_t g_persist_rows = 0;
 	int g_persist_blocks_per_sm = 1;
 	int g_persist_debug = 0; // timing experiments only: 1 = barriers without work, 2 = work without grid barriers
 	// launches with at least this many rows use the streaming kernels, smaller ones the preload
-	// kernels (measured cross-over on B200: ~1e5 rows, a third of a full wave of 148 SMs x 2048 threads)
-	int64_t g_stream_rows = 100000;
+	// kernels (measured cross-over on B200: between 1.4e5 and 8.8e5 rows per launch)
+	int64_t g_stream_rows = 200000;
 	// which streaming kernel shape the many-wave launches use (tuning knob). 2 = batches of 9 slots,
 	// 48 registers, 40 resident warps per SM: best of the sweep in profiles/r01_microbench_*.json
 	int g_stream_variant = 2;
@@ -86,14 +89,10 @@ namespace slabgpu {
 			__device__ __forceinline__ void chunk_load( const double * __restrict__ vals, const int32_t * __restrict__ cols,
 				int64_t at, int count, RowChunk & rc ) {
 				#pragma unroll
-				for( int k = 0; k < kChunk; ++k ) {
-					if( k < count ) {
-						rc.c[ k ] = __ldcs( cols + at + static_cast< int64_t >( k ) * kSlice );
-						rc.v[ k ] = __ldcs( vals + at + static_cast< int64_t >( k ) * kSlice );
-					} else {
-						rc.c[ k ] = -1;
-						rc.v[ k ] = 0.0;
-					}
+				for( int k = 0; k < kChunk; ++k ) { // predicated loads, no branches: slots beyond the slice read as padding
+					const bool in = k < count;
+					rc.c[ k ] = in ? __ldcs( cols + at + static_cast< int64_t >( k ) * kSlice ) : -1;
+					rc.v[ k ] = in ? __ldcs( vals + at + static_cast< int64_t >( k ) * kSlice ) : 0.0;
 				}
 			}
 
@@ -107,20 +106,20 @@ namespace slabgpu {
 				#pragma unroll
 				for( int k0 = 0; k0 < kChunk; k0 += kBatch ) {
 					double xv[ kBatch ];
+					// straight-line code: slots beyond `count` carry column -1 (chunk_load) and drop out
+					// through the same select as stored padding
 					#pragma unroll
 					for( int j = 0; j < kBatch; ++j ) {
 						const int k = k0 + j;
-						xv[ j ] = k < count ? x[ rc.c[ k ] < 0 ? 0 : rc.c[ k ] ] : 0.0;
+						xv[ j ] = x[ rc.c[ k ] < 0 ? 0 : rc.c[ k ] ];
 					}
 					#pragma unroll
 					for( int j = 0; j < kBatch; ++j ) {
 						const int k = k0 + j;
-						if( k < count ) {
-							const double sum = __dadd_rn( acc, __dmul_rn( rc.v[ k ], xv[ j ] ) );
-							acc = rc.c[ k ] < 0 ? acc : sum;
-							if( WANT_DIAG ) {
-								diag = rc.c[ k ] == diag_row ? rc.v[ k ] : diag;
-							}
+						const double sum = __dadd_rn( acc, __dmul_rn( rc.v[ k ], xv[ j ] ) );
+						acc = rc.c[ k ] < 0 ? acc : sum;
+						if( WANT_DIAG ) {
+							diag = rc.c[ k ] == diag_row ? rc.v[ k ] : diag;
 						}
 					}
 				}
@@ -554,29 +553,27 @@ namespace slabgpu {
 			//    row); the updated value also replaces the stale diagonal gather.
 			//  RESID (flags & 2): after the update, r_c[k] = 0 + 1*(1*r[i] + (-1)*(A z)[i]) with the NEW z[i] on
 			//    the diagonal (multigrid.hpp:100-104): all other colours are final in the last backward step.
-			__device__ __forceinline__ void persistent_row( const VcyclePhase & ph, int64_t k, int32_t i, const RowChunk & rc,
-				int width ) {
+			__device__ __forceinline__ void persistent_row( const VcyclePhase & ph, int64_t k, int32_t i, const RowChunk & rc ) {
 				double xv[ kChunk ];
 				#pragma unroll
 				for( int j = 0; j < kChunk; ++j ) {
-					xv[ j ] = j < width ? ph.z[ rc.c[ j ] < 0 ? 0 : rc.c[ j ] ] : 0.0;
+					xv[ j ] = ph.z[ rc.c[ j ] < 0 ? 0 : rc.c[ j ] ]; // slots beyond the width carry column -1
 				}
+				const bool prolong = ( ph.flags & 1 ) != 0;
 				double zi = ph.z[ i ];
 				const double ri = ph.r[ i ];
-				if( ph.flags & 1 ) {
+				if( prolong ) {
 					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, ph.src[ k ] ) );
 					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 				}
 				double s = 0.0, d = 0.0;
 				#pragma unroll
 				for( int j = 0; j < kChunk; ++j ) {
-					if( j < width ) {
-						const bool diagonal = rc.c[ j ] == i;
-						const double xj = ( ( ph.flags & 1 ) && diagonal ) ? zi : xv[ j ];
-						const double sum = __dadd_rn( s, __dmul_rn( rc.v[ j ], xj ) );
-						s = rc.c[ j ] < 0 ? s : sum;
-						d = diagonal ? rc.v[ j ] : d;
-					}
+					const bool diagonal = rc.c[ j ] == i;
+					const double xj = ( prolong && diagonal ) ? zi : xv[ j ];
+					const double sum = __dadd_rn( s, __dmul_rn( rc.v[ j ], xj ) );
+					s = rc.c[ j ] < 0 ? s : sum;
+					d = diagonal ? rc.v[ j ] : d;
 				}
 				const double znew = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
 				ph.z[ i ] = znew;
@@ -584,11 +581,9 @@ namespace slabgpu {
 					double az = 0.0;
 					#pragma unroll
 					for( int j = 0; j < kChunk; ++j ) {
-						if( j < width ) {
-							const double xj = rc.c[ j ] == i ? znew : xv[ j ];
-							const double sum = __dadd_rn( az, __dmul_rn( rc.v[ j ], xj ) );
-							az = rc.c[ j ] < 0 ? az : sum;
-						}
+						const double xj = rc.c[ j ] == i ? znew : xv[ j ];
+						const double sum = __dadd_rn( az, __dmul_rn( rc.v[ j ], xj ) );
+						az = rc.c[ j ] < 0 ? az : sum;
 					}
 					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
 					ph.out[ k ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
@@ -626,38 +621,59 @@ namespace slabgpu {
 				if( gtid < sph[ 0 ].count ) {
 					persistent_load( sph[ 0 ], gtid, row, rc, width );
 				}
+				long long t_work = 0, t_rest = 0, t_arrive = 0, t_pref = 0, t_wait = 0;
 				for( int p = 0; p < nphases; ++p ) {
 					const VcyclePhase & ph = sph[ p ];
+					const long long c0 = clock64();
 					if( gtid < ph.count && row >= 0 && debug != 1 ) {
-						persistent_row( ph, gtid, row, rc, width );
+						persistent_row( ph, gtid, row, rc );
 					}
+					const long long c1 = clock64();
 					for( int64_t k = gtid + gsize; k < ph.count; k += gsize ) { // phases larger than the grid
 						RowChunk extra;
 						int32_t i;
 						int w;
 						persistent_load( ph, k, i, extra, w );
 						if( i >= 0 ) {
-							persistent_row( ph, k, i, extra, w );
+							persistent_row( ph, k, i, extra );
 						}
 					}
 					for( int64_t k = gtid; k < ph.zero_count; k += gsize ) { // set_all(z_c, 0), multigrid.hpp:104
 						ph.zero[ k ] = 0.0;
 					}
+					const long long c2 = clock64();
 					if( p + 1 < nphases ) {
 						bool last = false;
 						if( debug != 2 ) {
 							grid_arrive( bar, gridDim.x, generation, last );
 						}
+						const long long c3 = clock64();
 						row = -1;
 						if( gtid < sph[ p + 1 ].count ) {
 							persistent_load( sph[ p + 1 ], gtid, row, rc, width ); // immutable data, overlaps the barrier
 						}
+						const long long c4 = clock64();
 						if( debug != 2 ) {
 							grid_wait( bar, generation, last );
 						} else {
 							__syncthreads();
 						}
+						const long long c5 = clock64();
+						t_work += c1 - c0;
+						t_rest += c2 - c1;
+						t_arrive += c3 - c2;
+						t_pref += c4 - c3;
+						t_wait += c5 - c4;
 					}
+				}
+				if( debug == 3 && gtid == 0 ) {
+					long long * out = reinterpret_cast< long long * >( bar + 40 );
+					out[ 0 ] = t_work;
+					out[ 1 ] = t_rest;
+					out[ 2 ] = t_arrive;
+					out[ 3 ] = t_pref;
+					out[ 4 ] = t_wait;
+					out[ 5 ] = nphases;
 				}
 			}
 

@@ -437,8 +437,8 @@ namespace slabgpu {
 		void prepare_persistent( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
 			slab_ctx_s * ctx = L->ctx;
 			if( ctx->d_barrier == nullptr ) {
-				SLAB_CUDA( cudaMalloc( &ctx->d_barrier, 64 * sizeof( unsigned int ) ) );
-				const unsigned int zeros[ 64 ] = { 0u };
+				SLAB_CUDA( cudaMalloc( &ctx->d_barrier, 128 * sizeof( unsigned int ) ) );
+				const unsigned int zeros[ 128 ] = { 0u };
 				upload_sync( ctx->stream, ctx->d_barrier, zeros, sizeof( zeros ) );
 			}
 			if( ctx->persist_grid == 0 ) {
