@@ -87,6 +87,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_use_pdl = value ? 1 : 0;
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
+		} else if( k == "l2_window" ) {
+			g_l2_window = static_cast< int >( value );
 		} else if( k == "persist_debug" ) {
 			g_persist_debug = static_cast< int >( value );
 		} else if( k == "persist_blocks_per_sm" ) {
@@ -151,6 +153,19 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_PERSIST_BLOCKS_PER_SM" ) ) {
 			g_persist_blocks_per_sm = std::atoi( v );
+		}
+		if( const char * v = std::getenv( "SLAB_L2_WINDOW" ) ) {
+			g_l2_window = std::atoi( v );
+		}
+		// L2 persisting carve-out for the vector that fine-level colour steps re-gather (kernels.cu)
+		if( prop.persistingL2CacheMaxSize > 0 && g_l2_window ) {
+			if( cudaDeviceSetLimit( cudaLimitPersistingL2CacheSize, static_cast< size_t >( prop.persistingL2CacheMaxSize ) )
+				== cudaSuccess ) {
+				g_l2_persist_bytes = static_cast< size_t >( prop.persistingL2CacheMaxSize );
+				g_l2_window_max = static_cast< size_t >( prop.accessPolicyMaxWindowSize );
+			} else {
+				cudaGetLastError();
+			}
 		}
 		std::unique_ptr< slab_ctx_s > ctx( new slab_ctx_s );
 		ctx->device = device;

@@ -65,10 +65,22 @@ namespace slabgpu {
 			}
 			op_dot_to_slot( r, z, S_RHO );                                        // cg.hpp:116
 			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
-			op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
-			op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
-			kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
-			op_dot_to_slot( r, r, S_RR );                                         // cg.hpp:132
+			if( ctx->dot_mode == SLAB_DOT_TREE ) {
+				// tree-dot mode: p'Ap rides on the product's epilogue and r'r on the x/r update — two
+				// passes over the vectors and two launches fewer per iteration
+				halo_exchange( H, p, -1 );
+				kern::spmv( st, H->A->sell.slice_off, H->A->sell.vals, H->A->sell.cols, p->d, q->d,
+					static_cast< int64_t >( H->n ), ctx->d_partials, ctx->d_counter, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
+				allreduce_slot( ctx, S_PQ );
+				kern::cg_update_xr_dot( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
+					ctx->d_counter );                                                 // cg.hpp:127-132
+				allreduce_slot( ctx, S_RR );
+			} else {
+				op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
+				op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
+				kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
+				op_dot_to_slot( r, r, S_RR );                                         // cg.hpp:132
+			}
 			kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
 		}
 
@@ -137,6 +149,9 @@ namespace slabgpu {
 		if( cfg->use_preconditioner && limit > 0 ) {
 			mg_vcycle_prepare( H, ws->z.get(), ws->r.get(), cfg->sweeps ); // before any capture
 		}
+		// reduction scratch for every dot shape used below (allocation is illegal while capturing)
+		ensure_partials( ctx, std::max< uint64_t >( std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
+			kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
 		if( graphs && limit > 0 ) {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
@@ -147,8 +162,8 @@ namespace slabgpu {
 					ws->iter_exec = nullptr;
 				}
 				// reduction scratch must exist before capture (allocation is illegal while capturing)
-				ensure_partials( ctx, std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
-					kern::dot_tree_blocks( n, ctx->sm_count ) ) );
+				ensure_partials( ctx, std::max< uint64_t >( std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
+					kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
 				cudaGraph_t graph = nullptr;
 				const uint64_t before = g_launch_count;
 				SLAB_CUDA( cudaStreamBeginCapture( st, cudaStreamCaptureModeThreadLocal ) );

@@ -56,6 +56,9 @@ namespace slabgpu {
 	extern int64_t g_persist_rows;   // levels whose largest colour has fewer rows run inside the persistent kernel (0 = off)
 	extern int g_persist_blocks_per_sm;
 	extern int g_persist_debug;
+	extern size_t g_l2_persist_bytes;
+	extern size_t g_l2_window_max;
+	extern int g_l2_window;
 	extern int64_t g_stream_rows;
 	extern int g_stream_variant;
 	extern uint64_t g_launch_count;

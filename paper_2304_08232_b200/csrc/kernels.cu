@@ -25,6 +25,13 @@ namespace slabgpu {
 
 	uint64_t g_launch_count = 0;
 	int g_use_pdl = 1;
+	// L2 persisting carve-out (set by slab_ctx_create from the device limits; 0 = unused)
+	size_t g_l2_persist_bytes = 0;
+	size_t g_l2_window_max = 0;
+	// attach an access-policy window on z to fine-level colour steps. OFF by default: measured on B200
+	// (tools/l2_window_probe.py) the carve-out helps the 192^3 sweep by 2.6% but costs 12-18% at 104^3 and
+	// 256^3, because it shrinks the L2 that everything else shares. Enable with SLAB_L2_WINDOW=1.
+	int g_l2_window = 0;
 	uint64_t g_tuning_epoch = 0;
 	// levels whose largest colour has fewer rows than this run inside the persistent V-cycle kernel.
 	// OFF by default: measured on B200 (tools/persistent_probe.py) a phase costs 3.1-4.2 us (release
@@ -51,6 +58,12 @@ namespace slabgpu {
 				return static_cast< unsigned int >( ( count + block - 1 ) / block );
 			}
 
+			// Vector that the next launch should keep in the L2 persisting carve-out (the z of a fine-level
+			// colour step: every step gathers all of it while the matrix streams through). Consumed by the
+			// next launch() only.
+			const void * t_window_base = nullptr;
+			size_t t_window_bytes = 0;
+
 			// launch with the programmatic-stream-serialization attribute (PDL)
 			template< class... KArgs, class... Args >
 			void launch( void ( *kernel )( KArgs... ), unsigned int grid, unsigned int block, cudaStream_t st,
@@ -60,11 +73,27 @@ namespace slabgpu {
 				cfg.blockDim = dim3( block, 1, 1 );
 				cfg.dynamicSmemBytes = 0;
 				cfg.stream = st;
-				cudaLaunchAttribute attr[ 1 ];
-				attr[ 0 ].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-				attr[ 0 ].val.programmaticStreamSerializationAllowed = 1;
+				cudaLaunchAttribute attr[ 2 ];
+				unsigned int count = 0;
+				if( g_use_pdl ) {
+					attr[ count ].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+					attr[ count ].val.programmaticStreamSerializationAllowed = 1;
+					++count;
+				}
+				if( t_window_base != nullptr && g_l2_persist_bytes > 0 ) {
+					const size_t bytes = t_window_bytes < g_l2_window_max ? t_window_bytes : g_l2_window_max;
+					attr[ count ].id = cudaLaunchAttributeAccessPolicyWindow;
+					attr[ count ].val.accessPolicyWindow.base_ptr = const_cast< void * >( t_window_base );
+					attr[ count ].val.accessPolicyWindow.num_bytes = bytes;
+					const double ratio = static_cast< double >( g_l2_persist_bytes ) / static_cast< double >( bytes );
+					attr[ count ].val.accessPolicyWindow.hitRatio = static_cast< float >( ratio < 1.0 ? ratio : 1.0 );
+					attr[ count ].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+					attr[ count ].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+					++count;
+				}
+				t_window_base = nullptr;
 				cfg.attrs = attr;
-				cfg.numAttrs = g_use_pdl ? 1 : 0;
+				cfg.numAttrs = count;
 				SLAB_CUDA( cudaLaunchKernelEx( &cfg, kernel, static_cast< KArgs >( args )... ) );
 				count_launch();
 			}
@@ -279,6 +308,22 @@ namespace slabgpu {
 				}
 			}
 
+			// one block folds `count` block partials in a fixed order (each thread a strided chain, then the tree)
+			__global__ void __launch_bounds__( 1024 ) k_sum_partials( const double * __restrict__ partials, uint64_t count,
+				double * out ) {
+				__shared__ double smem[ 32 ];
+				dep_trigger();
+				dep_wait();
+				double v = 0.0;
+				for( uint64_t b = threadIdx.x; b < count; b += blockDim.x ) {
+					v = __dadd_rn( v, partials[ b ] );
+				}
+				v = block_tree_sum( v, smem );
+				if( threadIdx.x == 0 ) {
+					*out = v;
+				}
+			}
+
 			__global__ void __launch_bounds__( kBlock ) k_dot_tree( const double * __restrict__ x,
 				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
 				__shared__ double smem[ 32 ];
@@ -311,7 +356,9 @@ namespace slabgpu {
 			template< bool MASKED >
 			__global__ void __launch_bounds__( kBlock ) k_spmv( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, const int32_t * __restrict__ members, int64_t count ) {
+				double * __restrict__ y, const int32_t * __restrict__ members, int64_t count, double * dot_partials,
+				unsigned int * dot_counter, double * dot_out ) {
+				__shared__ double smem[ 32 ];
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const bool live = k < count;
 				int64_t row = 0, begin = 0;
@@ -327,21 +374,37 @@ namespace slabgpu {
 				}
 				dep_trigger();
 				dep_wait();
-				if( !live ) {
-					return;
+				double prod = 0.0;
+				if( live ) {
+					double unused = 0.0;
+					double acc = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, x, 0.0, -1, unused );
+					acc = row_tail< false >( vals, cols, begin, width, x, acc, -1, unused );
+					y[ row ] = acc;
+					prod = dot_out != nullptr ? __dmul_rn( x[ row ], acc ) : 0.0;
 				}
-				double unused = 0.0;
-				double acc = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, x, 0.0, -1, unused );
-				acc = row_tail< false >( vals, cols, begin, width, x, acc, -1, unused );
-				y[ row ] = acc;
+				if( dot_out != nullptr ) { // x'(A x): block partials here, folded by k_sum_partials (cg.hpp:122-123)
+					const double block_sum = block_tree_sum( prod, smem );
+					if( threadIdx.x == 0 ) {
+						dot_partials[ blockIdx.x ] = block_sum;
+					}
+				}
 			}
 
 			// smoother.hpp:60-72 fused: s = row sum over z, then z[i] = ((r[i] - s) + z[i]*d) / d.
 			// Rows of one colour never neighbour each other, so reading z while other threads of
 			// the same launch write their own z[i] is race-free (coloring.hpp:165-204).
+			// Grid transfers ride on the colour-0 steps next to them (stencil levels: colour 0 == injected rows,
+			// position k of the colour-0 block == coarse row k):
+			//  flags & 1 — prolongation first (multigrid.hpp:71-81): z[i] <- 1*z[i] + 1*(0 + 1*src[k]); the
+			//    value is stored before the row sum, whose diagonal gather then reads it back;
+			//  flags & 2 — residual + restriction behind (multigrid.hpp:100-104), valid on the LAST backward
+			//    colour-0 step where every other colour is final: with the new z[i] stored, the ordered row sum
+			//    is taken again (matrix row still in registers) and out[k] = 0 + 1*(1*r[i] + (-1)*(A z)[i]);
+			//    zero[k] = 0 prepares the coarse guess (multigrid.hpp:104).
 			__global__ void __launch_bounds__( kBlock, 2 ) k_gs_color( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
+				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				int32_t i = -1;
 				int64_t begin = 0;
@@ -362,11 +425,24 @@ namespace slabgpu {
 					return;
 				}
 				const double ri = r[ i ];
+				double zi = z[ i ];
+				if( flags & 1 ) {
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ k ] ) );
+					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+					z[ i ] = zi;
+				}
 				double d = 0.0;
 				double s = chunk_accumulate< true >( rc, width < kChunk ? width : kChunk, z, 0.0, i, d );
 				s = row_tail< true >( vals, cols, begin, width, z, s, i, d );
-				const double zi = z[ i ];
 				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+				if( flags & 2 ) {
+					double unused = 0.0;
+					double az = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, z, 0.0, -1, unused );
+					az = row_tail< false >( vals, cols, begin, width, z, az, -1, unused );
+					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
+					out[ k ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+					zero[ k ] = 0.0;
+				}
 			}
 
 			// multigrid.hpp:100-104 fused on the injected rows (= the colour-0 block, whose p-th
@@ -374,7 +450,7 @@ namespace slabgpu {
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
-				double * __restrict__ r_c ) {
+				double * __restrict__ r_c, double * __restrict__ zero ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const bool live = p < n_coarse;
 				int32_t i = 0;
@@ -399,6 +475,9 @@ namespace slabgpu {
 				az = row_tail< false >( vals, cols, begin, width, z, az, -1, unused );
 				const double f = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -1.0, az ) );
 				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+				if( zero != nullptr ) {
+					zero[ p ] = 0.0; // set_all(z_c, 0), multigrid.hpp:104
+				}
 			}
 
 			// Batched streaming row sum: B (column, value) pairs are loaded together, then their B
@@ -428,7 +507,8 @@ namespace slabgpu {
 					double xv[ B ];
 					#pragma unroll
 					for( int j = 0; j < B; ++j ) {
-						xv[ j ] = COHERENT ? __ldcg( x + ( c[ j ] < 0 ? 0 : c[ j ] ) ) : x[ c[ j ] < 0 ? 0 : c[ j ] ];
+						const double * xp = x + ( c[ j ] < 0 ? 0 : c[ j ] );
+						xv[ j ] = COHERENT ? __ldcg( xp ) : *xp;
 					}
 					int32_t cc[ B ];
 					double vv[ B ];
@@ -460,7 +540,8 @@ namespace slabgpu {
 			template< int B, int MINBLOCKS >
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_batched( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r,
+				const double * __restrict__ src ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -472,9 +553,14 @@ namespace slabgpu {
 				if( i < 0 ) {
 					return;
 				}
+				double zi = z[ i ];
+				if( src != nullptr ) { // prolongation fused in front, see k_gs_color
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ k ] ) );
+					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+					z[ i ] = zi;
+				}
 				double d = 0.0;
 				const double s = row_sum_batched< B, true >( slice_off, vals, cols, pos, z, i, d );
-				const double zi = z[ i ];
 				const double ri = r[ i ];
 				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
 			}
@@ -482,15 +568,24 @@ namespace slabgpu {
 			template< int B, int MINBLOCKS >
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_spmv_batched( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, int64_t nrows ) {
+				double * __restrict__ y, int64_t nrows, double * dot_partials, unsigned int * dot_counter, double * dot_out ) {
+				__shared__ double smem[ 32 ];
 				dep_trigger();
 				dep_wait();
 				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( row >= nrows ) {
-					return;
+				double prod = 0.0;
+				if( row < nrows ) {
+					double unused = 0.0;
+					const double acc = row_sum_batched< B, false >( slice_off, vals, cols, row, x, -1, unused );
+					y[ row ] = acc;
+					prod = dot_out != nullptr ? __dmul_rn( x[ row ], acc ) : 0.0;
 				}
-				double unused = 0.0;
-				y[ row ] = row_sum_batched< B, false >( slice_off, vals, cols, row, x, -1, unused );
+				if( dot_out != nullptr ) { // x'(A x): block partials here, folded by k_sum_partials (cg.hpp:122-123)
+					const double block_sum = block_tree_sum( prod, smem );
+					if( threadIdx.x == 0 ) {
+						dot_partials[ blockIdx.x ] = block_sum;
+					}
+				}
 			}
 
 			// ---- persistent sub-V-cycle (coarse levels): phases separated by a grid barrier
@@ -716,7 +811,7 @@ namespace slabgpu {
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_stream( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
-				double * __restrict__ r_c ) {
+				double * __restrict__ r_c, double * __restrict__ zero ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -725,9 +820,12 @@ namespace slabgpu {
 				}
 				const int32_t i = rows[ p ];
 				double unused = 0.0;
-				const double az = row_sum_streaming< false >( slice_off, vals, cols, p, z, -1, unused );
+				const double az = row_sum_batched< 9, false >( slice_off, vals, cols, p, z, -1, unused );
 				const double f = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -1.0, az ) );
 				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+				if( zero != nullptr ) {
+					zero[ p ] = 0.0;
+				}
 			}
 
 			// multigrid.hpp:71-81 at the injected rows: f[i] = 0 + 1*z_c[p]; z[i] = 1*z[i] + 1*f[i].
@@ -778,6 +876,29 @@ namespace slabgpu {
 				if( i == 0 ) {
 					scalars[ S_RHO_PREV ] = rho; // cg.hpp:130 (nobody reads rho_prev in this launch)
 				}
+			}
+
+			// the same update with r'r (cg.hpp:132) reduced in the tree-dot shape on the way out
+			__global__ void __launch_bounds__( kBlock ) k_cg_update_xr_dot( double * x, double * r, const double * __restrict__ p,
+				const double * __restrict__ q, double * scalars, uint64_t n, double * partials, unsigned int * counter ) {
+				__shared__ double smem[ 32 ];
+				__shared__ bool is_last;
+				dep_trigger();
+				dep_wait();
+				const double rho = scalars[ S_RHO ];
+				const double alpha = __ddiv_rn( rho, scalars[ S_PQ ] );
+				double acc = 0.0;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				for( uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x; i < n; i += stride ) {
+					x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );
+					const double rn = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -alpha, q[ i ] ) );
+					r[ i ] = rn;
+					acc = __dadd_rn( acc, __dmul_rn( rn, rn ) );
+				}
+				if( blockIdx.x == 0 && threadIdx.x == 0 ) {
+					scalars[ S_RHO_PREV ] = rho;
+				}
+				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, scalars + S_RR, smem, &is_last );
 			}
 
 			__global__ void k_cg_record( const double * __restrict__ scalars, double * hist_rr, double * hist_pq,
@@ -836,36 +957,51 @@ namespace slabgpu {
 			launch( k_dot_tree, blocks, kBlock, st, x, y, n, partials, counter, out );
 		}
 
+		uint64_t spmv_dot_blocks( int64_t nrows ) {
+			return blocks_for( nrows > 0 ? nrows : 1 );
+		}
+
 		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, int64_t nrows ) {
+			const double * x, double * y, int64_t nrows, double * dot_partials, unsigned int * dot_counter,
+			double * dot_out ) {
 			if( nrows == 0 ) {
+				if( dot_out != nullptr ) {
+					launch( k_dot_empty, 1, 1, st, dot_out );
+				}
 				return;
 			}
 			if( nrows >= g_stream_rows ) {
 				const unsigned int grid = blocks_for( nrows );
 				switch( g_stream_variant ) {
 					case 1:
-						launch( k_spmv_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
 						break;
 					case 2:
-						launch( k_spmv_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
 						break;
 					case 3:
-						launch( k_spmv_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
 						break;
 					case 4:
-						launch( k_spmv_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
 						break;
 					case 5:
-						launch( k_spmv_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
 						break;
 					default:
-						launch( k_spmv_stream, grid, kBlock, st, slice_off, vals, cols, x, y, nrows );
+						launch( k_spmv_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, x, y, nrows, dot_partials, dot_counter, dot_out );
+				}
+				if( dot_out != nullptr ) {
+					launch( k_sum_partials, 1, 1024, st, static_cast< const double * >( dot_partials ), static_cast< uint64_t >( grid ), dot_out );
 				}
 				return;
 			}
 			launch( k_spmv< false >, blocks_for( nrows ), kBlock, st, slice_off, vals, cols, x, y,
-				static_cast< const int32_t * >( nullptr ), nrows );
+				static_cast< const int32_t * >( nullptr ), nrows, dot_partials, dot_counter, dot_out );
+			if( dot_out != nullptr ) {
+				launch( k_sum_partials, 1, 1024, st, static_cast< const double * >( dot_partials ),
+					static_cast< uint64_t >( blocks_for( nrows ) ), dot_out );
+			}
 		}
 
 		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
@@ -873,56 +1009,67 @@ namespace slabgpu {
 			if( count == 0 ) {
 				return;
 			}
-			launch( k_spmv< true >, blocks_for( count ), kBlock, st, slice_off, vals, cols, x, y, members, count );
+			launch( k_spmv< true >, blocks_for( count ), kBlock, st, slice_off, vals, cols, x, y, members, count,
+				static_cast< double * >( nullptr ), static_cast< unsigned int * >( nullptr ), static_cast< double * >( nullptr ) );
+		}
+
+		bool gs_color_step_can_fuse_residual( int64_t pos_count ) {
+			return pos_count < g_stream_rows; // the preload shape keeps the matrix row in registers
 		}
 
 		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r ) {
+			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
+			const double * src, double * out, double * zero, size_t window_bytes ) {
 			if( pos_count == 0 ) {
 				return;
 			}
 			if( pos_count >= g_stream_rows ) {
+				if( flags & 2 ) {
+					fail( SLAB_ERR_INTERNAL, "gs_color_step: the streaming shape cannot fuse the residual" );
+				}
+				const double * prolong = ( flags & 1 ) ? src : nullptr;
 				const unsigned int grid = blocks_for( pos_count );
+				if( g_l2_window && window_bytes > 0 ) {
+					t_window_base = z;
+					t_window_bytes = window_bytes;
+				}
 				switch( g_stream_variant ) {
 					case 1:
-						launch( k_gs_color_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
-						break;
-					case 2:
-						launch( k_gs_color_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
 						break;
 					case 3:
-						launch( k_gs_color_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
 						break;
 					case 4:
-						launch( k_gs_color_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
 						break;
 					case 5:
-						launch( k_gs_color_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
 						break;
 					case 6:
-						launch( k_gs_color, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, flags, src, out, zero );
 						break;
 					default:
-						launch( k_gs_color_stream, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r );
+						launch( k_gs_color_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
 				}
 				return;
 			}
 			launch( k_gs_color, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z,
-				r );
+				r, flags, src, out, zero );
 		}
 
 		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c ) {
+			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c, double * zero ) {
 			if( n_coarse == 0 ) {
 				return;
 			}
 			if( n_coarse >= g_stream_rows ) {
 				launch( k_residual_restrict_stream, blocks_for( n_coarse ), kBlock, st, slice_off, vals, cols, rows, n_coarse,
-					z, r, r_c );
+					z, r, r_c, zero );
 				return;
 			}
 			launch( k_residual_restrict, blocks_for( n_coarse ), kBlock, st, slice_off, vals, cols, rows, n_coarse, z, r,
-				r_c );
+				r_c, zero );
 		}
 
 		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c ) {
@@ -972,6 +1119,12 @@ namespace slabgpu {
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n ) {
 			launch( k_cg_update_xr, n == 0 ? 1u : blocks_for( n ), kBlock, st, x, r, p, q, scalars, n );
+		}
+
+		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
+			uint64_t n, int sm_count, double * partials, unsigned int * counter ) {
+			launch( k_cg_update_xr_dot, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
+				scalars, n, partials, counter );
 		}
 
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,

@@ -23,19 +23,30 @@ namespace slabgpu {
 			unsigned int * counter, double * out );
 
 		// ---- SELL-32 matrix-vector products (operations.hpp:116-125, :164-174)
+		// dot_out != nullptr additionally reduces x'(A x) in the tree-dot shape (cg.hpp:122-123 in one pass);
+		// dot_partials then needs spmv_dot_blocks(nrows) doubles
 		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, int64_t nrows );
+			const double * x, double * y, int64_t nrows, double * dot_partials = nullptr,
+			unsigned int * dot_counter = nullptr, double * dot_out = nullptr );
+		uint64_t spmv_dot_blocks( int64_t nrows );
 		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
 			const double * x, double * y, const int32_t * members, int64_t count );
 
 		// ---- fused Gauss-Seidel colour step (smoother.hpp:60-72) on the colour-major SELL
+		// flags bit 0: prolongation fused in front (z[i] += src[k], multigrid.hpp:71-81); bit 1: residual +
+		// restriction fused behind (out[k], zero[k] = 0; multigrid.hpp:100-104) — only where
+		// gs_color_step_can_fuse_residual(pos_count); both only on colour-0 steps of stencil levels.
 		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r );
+			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags = 0,
+			const double * src = nullptr, double * out = nullptr, double * zero = nullptr, size_t window_bytes = 0 );
+		// window_bytes > 0: size of z; many-wave launches then ask the L2 to keep z in its persisting carve-out
+		bool gs_color_step_can_fuse_residual( int64_t pos_count );
 
 		// ---- fused grid transfers (multigrid.hpp:100-104 and :71-81)
 		// r_c[p] = 0 + 1*( 1*r[i] + (-1)*(A z)[i] ),  i = rows[p], p in the colour-0 block = injected rows
 		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c );
+			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c,
+			double * zero = nullptr ); // zero: the coarse guess, cleared by the same threads (multigrid.hpp:104)
 		// z[i] = 1*z[i] + 1*(0 + 1*z_c[p]) at the injected rows
 		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c );
 
@@ -69,6 +80,9 @@ namespace slabgpu {
 		// alpha = rho/pq; x = 1*x + alpha*p; r = 1*r + (-alpha)*q; rho_prev <- rho
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n );
+		// the same plus r'r -> scalars[S_RR] (cg.hpp:132) in the tree-dot shape; partials: dot_tree_blocks doubles
+		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
+			uint64_t n, int sm_count, double * partials, unsigned int * counter );
 		// hist_rr[it] = rr, hist_pq[it] = pq, ++it
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,
 			unsigned int * iter_counter );

@@ -246,9 +246,11 @@ namespace slabgpu {
 		// One colour step. Invariant on distributed levels: the ghost copies of z are current on
 		// entry; the step then sends the just-updated boundary values of colour k to the neighbours
 		// (only that colour moved), which restores the invariant for the next step.
-		void color_step_enqueue( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r ) {
+		void color_step_enqueue( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r, int flags = 0 ) {
 			kern::gs_color_step( L->ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
-				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z->d, r->d );
+				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z->d, r->d, flags,
+				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr,
+				static_cast< size_t >( z->n_alloc ) * sizeof( double ) );
 			halo_exchange( L, z, static_cast< int >( k ) );
 		}
 
@@ -502,30 +504,55 @@ namespace slabgpu {
 			}
 			return;
 		}
-		symmetric_enqueue( L, z, r, sweeps );
 		if( !L->coarser ) {
+			symmetric_enqueue( L, z, r, sweeps );
 			if( count_stats ) {
 				L->stats.nnz_visited += 2 * sweeps * L->nnz;
 			}
 			return;
 		}
-		if( ctx->fused_transfers ) {
-			kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
-				static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d );
-		} else {
+		if( !ctx->fused_transfers || !L->is_stencil ) {
+			// the reference's composition, primitive by primitive (multigrid.hpp:94-111)
+			symmetric_enqueue( L, z, r, sweeps );
 			op_mxv( L->f.get(), nullptr, L->A.get(), z, SLAB_DESC_NONE ); // f <- A z
 			op_waxpby( L->f.get(), 1.0, r, -1.0, L->f.get() );            // f <- r - f
 			op_mxv( L->r_c.get(), nullptr, L->R.get(), L->f.get(), SLAB_DESC_NONE );
-		}
-		op_set_all( L->z_c.get(), 0.0 );
-		mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
-		if( ctx->fused_transfers ) {
-			kern::prolong_add( ctx->stream, L->d_rows, static_cast< int64_t >( L->z_c->n ), z->d, L->z_c->d );
-		} else {
+			op_set_all( L->z_c.get(), 0.0 );
+			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
 			op_mxv( L->f.get(), nullptr, L->R.get(), L->z_c.get(), SLAB_DESC_TRANSPOSE );
 			op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+			symmetric_enqueue( L, z, r, sweeps );
+		} else {
+			// Fused transfers. On a stencil level colour 0 is exactly the injected rows, in coarse-index
+			// order. The residual + restriction (and the zeroing of the coarse guess) ride on the LAST
+			// colour step of the pre-smoother — backward, colour 0, every other colour final — when that
+			// launch keeps its matrix rows in registers, else they are one extra pass over the colour-0
+			// rows; the prolongation rides on the FIRST colour step of the post-smoother (forward, colour
+			// 0), which reads no other colour-0 value. Results are bit-identical to the composition above.
+			const bool fuse_residual = kern::gs_color_step_can_fuse_residual( static_cast< int64_t >( L->color_size[ 0 ] ) );
+			const bool ghosts = L->z_c->n_alloc > L->z_c->n; // distributed: the ghost tail must be zeroed too
+			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
+				forward_enqueue( L, z, r );
+				for( uint64_t k = L->num_colors; k > 0; --k ) {
+					const bool last = sweep + 1 == sweeps && k == 1;
+					color_step_enqueue( L, k - 1, z, r, last && fuse_residual ? 2 : 0 );
+				}
+			}
+			if( !fuse_residual ) {
+				kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+					static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d, L->z_c->d );
+			}
+			if( ghosts ) {
+				op_set_all( L->z_c.get(), 0.0 );
+			}
+			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
+			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
+				for( uint64_t k = 0; k < L->num_colors; ++k ) {
+					color_step_enqueue( L, k, z, r, sweep == 0 && k == 0 ? 1 : 0 );
+				}
+				backward_enqueue( L, z, r );
+			}
 		}
-		symmetric_enqueue( L, z, r, sweeps );
 		if( count_stats ) {
 			L->stats.nnz_visited += 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz;
 		}
