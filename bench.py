@@ -390,10 +390,13 @@ def main():
         gs_ms = ctx.timer_stop()
         per_launch_s = gs_ms * 1e-3 / (16 * reps)
         achieved = gs_step_bytes(dims) / per_launch_s / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_gs_color (finest level colour step)", "achieved": achieved,
-                    "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic(dims),
-                    "algorithmic_bytes_per_launch": gs_step_bytes(dims), "us_per_launch": per_launch_s * 1e6,
-                    "peak_source": peak_src}
+        roofline = {"bound": "hbm", "kernel": "k_gs_color_batched<9,5> (finest-level colour step, smoother.hpp:60-72)",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": measured_traffic(dims), "algorithmic_bytes_per_launch": gs_step_bytes(dims),
+                    "us_per_launch": per_launch_s * 1e6, "launches_per_step": 32 * CG_ITERS,
+                    "share_of_step": 32 * CG_ITERS * per_launch_s * 1e3 / ms_per_step, "peak_source": peak_src,
+                    "how": "16 launches of one symmetric sweep timed alone with CUDA events on the library stream, "
+                           "10 repetitions after 3 warm-ups; traffic = dram bytes per launch from profiles/r01_ncu_gs_color_192.txt"}
 
     line = {
         "metric": "hpcg_gflops", "value": main_run["gflops"], "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,

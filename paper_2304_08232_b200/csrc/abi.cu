@@ -1,5 +1,7 @@
 // abi.cu — the extern "C" surface declared in include/slab_b200.h. Every entry point
 // translates internal exceptions into status codes; argument checks precede any work.
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -109,6 +111,68 @@ int slab_debug_read_barrier_words( slab_ctx_t ctx, long long * out6 ) {
 		}
 		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
 		SLAB_CUDA( cudaMemcpy( out6, ctx->d_barrier + 40, 6 * sizeof( long long ), cudaMemcpyDeviceToHost ) );
+	} );
+}
+
+// timing experiment: one symmetric sweep with colour-major vectors; returns ms per sweep and, in
+// *max_diff, the largest |difference| to the natural-layout sweep on the same data (must be 0)
+int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, int reps, double * ms, double * max_diff ) {
+	return guarded( [ & ] {
+		need( level, "slab_debug_playout_sweep" );
+		slab_ctx_s * ctx = level->ctx;
+		bind( ctx );
+		cudaStream_t st = ctx->stream;
+		const int64_t npos = level->color_pos[ level->num_colors ];
+		const int64_t entries = level->colorA.entries;
+		int32_t * nat2pos = nullptr;
+		int32_t * pcols = nullptr;
+		double * zp = nullptr;
+		double * rp = nullptr;
+		SLAB_CUDA( cudaMalloc( &nat2pos, level->n * sizeof( int32_t ) ) );
+		SLAB_CUDA( cudaMalloc( &pcols, entries * sizeof( int32_t ) ) );
+		SLAB_CUDA( cudaMalloc( &zp, npos * sizeof( double ) ) );
+		SLAB_CUDA( cudaMalloc( &rp, npos * sizeof( double ) ) );
+		kern::proto_invert_rows( st, level->d_rows, npos, nat2pos );
+		kern::proto_permute_cols( st, level->colorA.cols, nat2pos, entries, pcols );
+		kern::proto_gather_to_pos( st, level->d_rows, npos, z->d, zp );
+		kern::proto_gather_to_pos( st, level->d_rows, npos, r->d, rp );
+		const auto sweep = [ & ]() {
+			for( uint64_t k = 0; k < level->num_colors; ++k ) {
+				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k ],
+					static_cast< int64_t >( level->color_size[ k ] ), zp, rp );
+			}
+			for( uint64_t k = level->num_colors; k > 0; --k ) {
+				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k - 1 ],
+					static_cast< int64_t >( level->color_size[ k - 1 ] ), zp, rp );
+			}
+		};
+		sweep(); // one sweep to compare
+		rbgs_symmetric( level, z, r, 1 );
+		std::vector< double > a( npos ), b( level->n );
+		SLAB_CUDA( cudaMemcpyAsync( a.data(), zp, npos * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+		SLAB_CUDA( cudaMemcpyAsync( b.data(), z->d, level->n * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+		std::vector< int32_t > rows( npos );
+		SLAB_CUDA( cudaMemcpyAsync( rows.data(), level->d_rows, npos * sizeof( int32_t ), cudaMemcpyDeviceToHost, st ) );
+		SLAB_CUDA( cudaStreamSynchronize( st ) );
+		double diff = 0.0;
+		for( int64_t p = 0; p < npos; ++p ) {
+			if( rows[ p ] >= 0 ) {
+				diff = std::max( diff, std::abs( a[ p ] - b[ rows[ p ] ] ) );
+			}
+		}
+		if( max_diff ) *max_diff = diff;
+		for( int w = 0; w < 3; ++w ) sweep();
+		SLAB_CUDA( cudaEventRecord( ctx->timer_start, st ) );
+		for( int w = 0; w < reps; ++w ) sweep();
+		SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
+		SLAB_CUDA( cudaEventSynchronize( ctx->timer_stop ) );
+		float t = 0.0f;
+		SLAB_CUDA( cudaEventElapsedTime( &t, ctx->timer_start, ctx->timer_stop ) );
+		if( ms ) *ms = t / reps;
+		cudaFree( nat2pos );
+		cudaFree( pcols );
+		cudaFree( zp );
+		cudaFree( rp );
 	} );
 }
 

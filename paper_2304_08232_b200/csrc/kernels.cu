@@ -911,7 +911,62 @@ namespace slabgpu {
 				*iter_counter = it + 1;
 			}
 
+			// ---- prototype: colour-major ("P") vector layout. Vector entry of row position p lives at p.
+			__global__ void k_permute_cols( const int32_t * __restrict__ cols, const int32_t * __restrict__ nat2pos,
+				int64_t entries, int32_t * __restrict__ out ) {
+				const int64_t e = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( e < entries ) {
+					const int32_t c = cols[ e ];
+					out[ e ] = c < 0 ? -1 : nat2pos[ c ];
+				}
+			}
+			__global__ void k_invert_rows( const int32_t * __restrict__ rows, int64_t npos, int32_t * __restrict__ nat2pos ) {
+				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( p < npos && rows[ p ] >= 0 ) {
+					nat2pos[ rows[ p ] ] = static_cast< int32_t >( p );
+				}
+			}
+			__global__ void k_gather_to_pos( const int32_t * __restrict__ rows, int64_t npos, const double * __restrict__ nat,
+				double * __restrict__ pos ) {
+				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( p < npos ) {
+					pos[ p ] = rows[ p ] >= 0 ? nat[ rows[ p ] ] : 0.0;
+				}
+			}
+			template< int B, int MINBLOCKS >
+			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_pos( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ pcols, int64_t pos_begin, int64_t pos_count,
+				double * z, const double * __restrict__ r ) {
+				dep_trigger();
+				dep_wait();
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( k >= pos_count ) {
+					return;
+				}
+				const int64_t pos = pos_begin + k;
+				double d = 0.0;
+				const double s = row_sum_batched< B, true >( slice_off, vals, pcols, pos, z, static_cast< int32_t >( pos ), d );
+				const double zi = z[ pos ];
+				const double ri = r[ pos ];
+				z[ pos ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+			}
+
 		} // namespace
+
+		// prototype entry points (tools/playout_probe.py)
+		void proto_permute_cols( cudaStream_t st, const int32_t * cols, const int32_t * nat2pos, int64_t entries, int32_t * out ) {
+			k_permute_cols<<< blocks_for( entries ), kBlock, 0, st >>>( cols, nat2pos, entries, out );
+		}
+		void proto_invert_rows( cudaStream_t st, const int32_t * rows, int64_t npos, int32_t * nat2pos ) {
+			k_invert_rows<<< blocks_for( npos ), kBlock, 0, st >>>( rows, npos, nat2pos );
+		}
+		void proto_gather_to_pos( cudaStream_t st, const int32_t * rows, int64_t npos, const double * nat, double * pos ) {
+			k_gather_to_pos<<< blocks_for( npos ), kBlock, 0, st >>>( rows, npos, nat, pos );
+		}
+		void proto_gs_color_pos( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * pcols,
+			int64_t pos_begin, int64_t pos_count, double * z, const double * r ) {
+			launch( k_gs_color_pos< 9, 5 >, blocks_for( pos_count ), kBlock, st, slice_off, vals, pcols, pos_begin, pos_count, z, r );
+		}
 
 		// ================================================================ wrappers
 

@@ -73,6 +73,13 @@ namespace slabgpu {
 		void vcycle_persistent( cudaStream_t st, const VcyclePhase * d_phases, int nphases, unsigned int * d_barrier,
 			int grid_blocks );
 
+		// ---- prototype of the colour-major vector layout (timing experiments only)
+		void proto_permute_cols( cudaStream_t st, const int32_t * cols, const int32_t * nat2pos, int64_t entries, int32_t * out );
+		void proto_invert_rows( cudaStream_t st, const int32_t * rows, int64_t npos, int32_t * nat2pos );
+		void proto_gather_to_pos( cudaStream_t st, const int32_t * rows, int64_t npos, const double * nat, double * pos );
+		void proto_gs_color_pos( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * pcols,
+			int64_t pos_begin, int64_t pos_count, double * z, const double * r );
+
 		// ---- CG vector updates with device-resident scalars (cg.hpp:116-132)
 		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,

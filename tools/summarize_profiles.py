@@ -1,0 +1,109 @@
+#!/usr/bin/env python
+"""Turns the raw ncu outputs in gpurun_out/ into the committed summaries under profiles/:
+
+  profiles/r01_launches_<workload>.csv / .md   per-kernel device time and share of a CG iteration
+  profiles/r01_ncu_<kernel>_<workload>.txt     key metrics of one `ncu --set full` capture
+  profiles/traffic.json                        dram bytes per launch (bench.py's roofline.traffic)
+
+Usage: python tools/summarize_profiles.py   (no GPU needed; reads .ncu-rep with `ncu -i`)
+"""
+import collections
+import csv
+import json
+import os
+import re
+import shutil
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def launch_list(name, workload):
+    src = os.path.join(OUT, name)
+    if not os.path.exists(src):
+        return
+    shutil.copy(src, os.path.join(PROF, name))
+    with open(src) as fh:
+        lines = [l for l in fh if not l.startswith("==")]
+    rows = []
+    for r in csv.DictReader(lines):
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        kernel = re.sub(r"\(.*", "", r["Kernel Name"]).split("::")[-1]
+        value = float(r["Metric Value"].replace(",", ""))
+        rows.append((kernel, r["Grid Size"], value / 1000.0 if r["Metric Unit"].startswith("n") else value))
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for kernel, grid, us in rows:
+        agg[(kernel, grid)][0] += 1
+        agg[(kernel, grid)][1] += us
+    total = sum(v[1] for v in agg.values())
+    by_kernel = collections.defaultdict(float)
+    for (kernel, _grid), v in agg.items():
+        by_kernel[kernel] += v[1]
+    out = [f"# ncu launch list — {workload} ({len(rows)} launches captured, ≈3 CG iterations)",
+           "", "`ncu --metrics gpu__time_duration.sum --clock-control none` on `bench.py`; per-launch times are cold-cache and",
+           "serialised (ncu flushes caches and drops the programmatic overlap), so read the SHARES, not the absolutes.", "",
+           "| kernel | grid | launches | total µs | avg µs | share |", "|---|---|---|---|---|---|"]
+    for (kernel, grid), v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| {kernel} | {grid} | {v[0]} | {v[1]:.1f} | {v[1] / v[0]:.2f} | {v[1] / total * 100:.1f} % |")
+    out += ["", "| kernel (all grids) | share |", "|---|---|"]
+    for kernel, us in sorted(by_kernel.items(), key=lambda kv: -kv[1]):
+        out.append(f"| {kernel} | {us / total * 100:.1f} % |")
+    with open(os.path.join(PROF, name.replace(".csv", ".md")), "w") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "smsp__inst_executed.sum",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_tensor.sum"]
+
+
+def full_capture(rep, label, traffic_key, traffic):
+    src = os.path.join(OUT, rep)
+    if not os.path.exists(src):
+        return
+    raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    out = [f"ncu --set full --clock-control none --import-source on ({rep}), cold cache (ncu default cache control)", ""]
+    total = []
+    for r in rows[2:]:
+        out.append(f"kernel {r[hdr.index('Kernel Name')][:80]}  grid {r[hdr.index('Grid Size')]}  block {r[hdr.index('Block Size')]}")
+        for w in WANT:
+            if w in hdr:
+                i = hdr.index(w)
+                out.append(f"   {w:78s} {r[i]:>16s} {units[i]}")
+        rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
+        wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
+        scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}
+        total.append(rd * scale[units[hdr.index("dram__bytes_read.sum")]] + wr * scale[units[hdr.index("dram__bytes_write.sum")]])
+        out.append("")
+    with open(os.path.join(PROF, label), "w") as fh:
+        fh.write("\n".join(out) + "\n")
+    if total:
+        traffic.setdefault(traffic_key[0], {})[traffic_key[1]] = sum(total) / len(total)
+
+
+def main():
+    os.makedirs(PROF, exist_ok=True)
+    launch_list("r01_launches_hpcg192.csv", "hpcg192 (192^3, 4 levels)")
+    launch_list("r01_launches_hpcg104.csv", "hpcg104 (104^3, 4 levels)")
+    traffic = {}
+    tpath = os.path.join(PROF, "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath))
+    full_capture("r01_prof_gs_192.ncu-rep", "r01_ncu_gs_color_192.txt", ("gs_color_step", "192x192x192"), traffic)
+    full_capture("r01_prof_spmv_192.ncu-rep", "r01_ncu_spmv_192.txt", ("spmv", "192x192x192"), traffic)
+    with open(tpath, "w") as fh:
+        json.dump(traffic, fh, indent=1)
+    print(json.dumps(traffic))
+
+
+if __name__ == "__main__":
+    main()
