@@ -83,6 +83,11 @@ int slab_ctx_set_graphs( slab_ctx_t ctx, int enabled );
 /* fuse residual+restriction and prolongation+update (default 1); 0 runs the reference's
  * primitive-by-primitive composition (multigrid.hpp:100-104, :76-77) */
 int slab_ctx_set_fused_transfers( slab_ctx_t ctx, int enabled );
+/* LevelStats timing (problem.hpp:204-209, the monotonic_ns wrappers of smoother.hpp:79-98 and
+ * multigrid.hpp:50-53,75-79,92-114): when enabled, V-cycles run launch by launch with CUDA events around the
+ * same sections, and smoother_ns / transfer_ns / mg_ns are filled (device time). Off by default: the fast
+ * path replays CUDA graphs, where only nnz_visited is maintained. */
+int slab_ctx_set_profiling( slab_ctx_t ctx, int enabled );
 /* device-side elapsed time between two marks on the context's stream, milliseconds */
 int slab_ctx_timer_start( slab_ctx_t ctx );
 int slab_ctx_timer_stop( slab_ctx_t ctx, double * elapsed_ms );

@@ -15,6 +15,7 @@
  */
 #pragma once
 
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <memory>
@@ -538,6 +539,35 @@ namespace slab_b200 {
 		return out;
 	}
 
+	// ---- bench.hpp:53-105 — the HPCG symmetry test (caller of the hot path)
+	struct SymmetryReport { // report.hpp:63-75
+		bool skipped = false;
+		bool matrix_pass = false;
+		double matrix_diff = 0.0;
+		bool precond_pass = false;
+		double precond_diff = 0.0;
+		double tolerance = 0.0;
+		bool all_pass() const noexcept {
+			return skipped || ( matrix_pass && precond_pass );
+		}
+	};
+	inline double symmetry_tolerance( const DenseVector & x, const DenseVector & y ) { // bench.hpp:53-57
+		const double nx = std::sqrt( dot( x, x ) );
+		const double ny = std::sqrt( dot( y, y ) );
+		return 1e-8 * nx * ny * 26.0 * std::sqrt( static_cast< double >( x.size() ) );
+	}
+	namespace detail {
+		template< class Apply >
+		inline double bilinear_asymmetry( Context & ctx, Apply && apply, const DenseVector & x, const DenseVector & y ) {
+			DenseVector tmp( ctx, x.size() ); // bench.hpp:63-70
+			apply( tmp, y );
+			const double lhs = dot( x, tmp );
+			apply( tmp, x );
+			const double rhs = dot( y, tmp );
+			return std::abs( lhs - rhs );
+		}
+	} // namespace detail
+
 	// ---- rng.hpp:35-65 (host generator, then upload)
 	class Lcg64 {
 	public:
@@ -562,6 +592,30 @@ namespace slab_b200 {
 			host[ i ] = rng.next_symmetric();
 		}
 		return DenseVector::from( ctx, host );
+	}
+
+	/** bench.hpp:80-105: operator and V-cycle must act symmetrically on two LCG vectors. */
+	inline SymmetryReport symmetry_test( Context & ctx, ProblemLevel & hierarchy, std::uint64_t seed,
+		const SmootherConfig & smoother_cfg = {} ) {
+		const std::size_t n = hierarchy.n();
+		Lcg64 rng( seed );
+		const DenseVector x = random_vector( ctx, n, rng );
+		const DenseVector y = random_vector( ctx, n, rng );
+		SymmetryReport out;
+		out.tolerance = symmetry_tolerance( x, y );
+		const SparseMatrix A = hierarchy.A();
+		out.matrix_diff = detail::bilinear_asymmetry(
+			ctx, [ &A ]( DenseVector & result, const DenseVector & in ) { mxv( result, A, in ); }, x, y );
+		out.matrix_pass = out.matrix_diff <= out.tolerance;
+		out.precond_diff = detail::bilinear_asymmetry(
+			ctx,
+			[ &hierarchy, &smoother_cfg ]( DenseVector & result, const DenseVector & in ) {
+				set_all( result, 0.0 );
+				mg_vcycle( hierarchy, result, in, smoother_cfg );
+			},
+			x, y );
+		out.precond_pass = out.precond_diff <= out.tolerance;
+		return out;
 	}
 
 } // namespace slab_b200

@@ -106,6 +106,7 @@ SIGNATURES = {
     "slab_ctx_get_dot_mode": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "slab_ctx_set_graphs": (C.c_int, [_vp, C.c_int]),
     "slab_ctx_set_fused_transfers": (C.c_int, [_vp, C.c_int]),
+    "slab_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "slab_ctx_timer_start": (C.c_int, [_vp]),
     "slab_ctx_timer_stop": (C.c_int, [_vp, _pf64]),
     "slab_ctx_device_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), _pu64]),
@@ -289,6 +290,10 @@ class Context:
 
     def set_fused_transfers(self, enabled: bool) -> None:
         _check(_lib.slab_ctx_set_fused_transfers(self._h, int(enabled)))
+
+    def set_profiling(self, enabled: bool) -> None:
+        """LevelStats times (smoother_ns, transfer_ns, mg_ns) are only filled while this is on."""
+        _check(_lib.slab_ctx_set_profiling(self._h, int(enabled)))
 
     def timer_start(self) -> None:
         _check(_lib.slab_ctx_timer_start(self._h))

@@ -261,6 +261,10 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		cudaSetDevice( ctx->device );
 		cudaStreamSynchronize( ctx->stream );
 		dist_destroy( ctx );
+		spans_discard( ctx );
+		for( cudaEvent_t e : ctx->event_pool ) {
+			cudaEventDestroy( e );
+		}
 		cudaFree( ctx->d_scalars );
 		cudaFree( ctx->d_partials );
 		cudaFree( ctx->d_counter );
@@ -305,6 +309,15 @@ int slab_ctx_set_graphs( slab_ctx_t ctx, int enabled ) {
 	return guarded( [ & ] {
 		need( ctx, "slab_ctx_set_graphs" );
 		ctx->use_graphs = enabled ? 1 : 0;
+	} );
+}
+
+int slab_ctx_set_profiling( slab_ctx_t ctx, int enabled ) {
+	return guarded( [ & ] {
+		need( ctx, "slab_ctx_set_profiling" );
+		bind( ctx );
+		spans_resolve( ctx );
+		ctx->profiling = enabled ? 1 : 0;
 	} );
 }
 
@@ -665,6 +678,7 @@ int slab_level_destroy( slab_level_t level ) {
 		if( level ) {
 			cudaSetDevice( level->ctx->device );
 			cudaStreamSynchronize( level->ctx->stream );
+			spans_discard( level->ctx ); // pending intervals may point into this level's counters
 			delete level;
 		}
 	} );
@@ -759,6 +773,8 @@ int slab_level_stats_get( slab_level_t level, slab_level_stats * out ) {
 	return guarded( [ & ] {
 		need( level, "slab_level_stats_get" );
 		need( out, "slab_level_stats_get" );
+		bind( level->ctx );
+		spans_resolve( level->ctx ); // pending device-time intervals land in the counters now
 		*out = level->stats;
 	} );
 }
@@ -766,6 +782,8 @@ int slab_level_stats_get( slab_level_t level, slab_level_stats * out ) {
 int slab_level_stats_reset( slab_level_t level ) {
 	return guarded( [ & ] {
 		need( level, "slab_level_stats_reset" );
+		bind( level->ctx );
+		spans_resolve( level->ctx );
 		for( slab_level_s * at = level; at; at = at->coarser.get() ) {
 			at->stats = slab_level_stats{};
 		}

@@ -145,7 +145,7 @@ namespace slabgpu {
 		const uint64_t limit = already_converged ? 0 : planned;
 
 		// iteration graph, cached per (x, config)
-		const bool graphs = ctx->use_graphs != 0;
+		const bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
 			mg_vcycle_prepare( H, ws->z.get(), ws->r.get(), cfg->sweeps ); // before any capture
 		}

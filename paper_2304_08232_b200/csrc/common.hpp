@@ -92,8 +92,23 @@ namespace slabgpu {
 
 } // namespace slabgpu
 
+namespace slabgpu {
+	// a device-time interval whose length is added (or subtracted) to a LevelStats counter once resolved
+	struct TimedSpan {
+		cudaEvent_t begin, end;
+		uint64_t * target;
+		int sign;
+	};
+} // namespace slabgpu
+
 struct slab_ctx_s {
 	slabgpu::DistState * dist = nullptr; // null: single-process context
+	// LevelStats timing (problem.hpp:204-209): when on, V-cycles run launch by launch (no graphs, no
+	// fusion across the reference's categories) with CUDA events around the sections the reference
+	// wraps with its monotonic clock; intervals are resolved lazily when the stats are read
+	int profiling = 0;
+	std::vector< slabgpu::TimedSpan > spans;
+	std::vector< cudaEvent_t > event_pool;
 	int device = 0;
 	cudaStream_t stream = nullptr;
 	int sm_count = 0;
@@ -256,6 +271,8 @@ namespace slabgpu {
 	// everything mg_vcycle_enqueue needs that may allocate or copy (phase lists of the persistent kernel,
 	// lazily built transposes): must run before stream capture begins
 	void mg_vcycle_prepare( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
+	void spans_resolve( slab_ctx_s * ctx ); // synchronises; adds every pending interval to its counter
+	void spans_discard( slab_ctx_s * ctx );
 
 	// ---- ops (kernels.cu)
 	void op_set_all( slab_vec_s * v, double value );

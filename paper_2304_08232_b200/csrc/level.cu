@@ -22,6 +22,71 @@ slab_level_s::~slab_level_s() {
 
 namespace slabgpu {
 
+	// ---------------------------------------------------------------- LevelStats timing
+
+	namespace {
+		cudaEvent_t event_get( slab_ctx_s * ctx ) {
+			if( !ctx->event_pool.empty() ) {
+				cudaEvent_t e = ctx->event_pool.back();
+				ctx->event_pool.pop_back();
+				return e;
+			}
+			cudaEvent_t e = nullptr;
+			SLAB_CUDA( cudaEventCreate( &e ) );
+			return e;
+		}
+
+		// records the interval [construction, destruction) on the context's stream when profiling is on
+		struct Span {
+			slab_ctx_s * ctx;
+			uint64_t * target;
+			int sign;
+			cudaEvent_t begin = nullptr;
+			Span( slab_ctx_s * c, uint64_t * t, int s = 1 ) : ctx( c ), target( t ), sign( s ) {
+				if( ctx->profiling ) {
+					begin = event_get( ctx );
+					SLAB_CUDA( cudaEventRecord( begin, ctx->stream ) );
+				}
+			}
+			~Span() {
+				if( begin != nullptr ) {
+					cudaEvent_t end = event_get( ctx );
+					cudaEventRecord( end, ctx->stream );
+					ctx->spans.push_back( { begin, end, target, sign } );
+				}
+			}
+		};
+	} // namespace
+
+	void spans_resolve( slab_ctx_s * ctx ) {
+		if( ctx->spans.empty() ) {
+			return;
+		}
+		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
+		for( const TimedSpan & span : ctx->spans ) {
+			float ms = 0.0f;
+			if( cudaEventElapsedTime( &ms, span.begin, span.end ) == cudaSuccess ) {
+				const uint64_t ns = static_cast< uint64_t >( static_cast< double >( ms ) * 1e6 );
+				if( span.sign > 0 ) {
+					*span.target += ns;
+				} else {
+					*span.target -= ns < *span.target ? ns : *span.target;
+				}
+			}
+			ctx->event_pool.push_back( span.begin );
+			ctx->event_pool.push_back( span.end );
+		}
+		ctx->spans.clear();
+	}
+
+	void spans_discard( slab_ctx_s * ctx ) {
+		for( const TimedSpan & span : ctx->spans ) {
+			ctx->event_pool.push_back( span.begin );
+			ctx->event_pool.push_back( span.end );
+		}
+		ctx->spans.clear();
+	}
+
 	namespace {
 
 		int64_t round_up( int64_t v, int64_t m ) {
@@ -287,14 +352,20 @@ namespace slabgpu {
 	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
 		check_smoother_args( L, z, r );
 		halo_exchange( L, z, -1 );
-		forward_enqueue( L, z, r );
+		{
+			Span timed( L->ctx, &L->stats.smoother_ns ); // smoother.hpp:79,83
+			forward_enqueue( L, z, r );
+		}
 		L->stats.nnz_visited += L->nnz;
 	}
 
 	void rbgs_backward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {
 		check_smoother_args( L, z, r );
 		halo_exchange( L, z, -1 );
-		backward_enqueue( L, z, r );
+		{
+			Span timed( L->ctx, &L->stats.smoother_ns ); // smoother.hpp:94,98
+			backward_enqueue( L, z, r );
+		}
 		L->stats.nnz_visited += L->nnz;
 	}
 
@@ -304,7 +375,10 @@ namespace slabgpu {
 		}
 		check_smoother_args( L, z, r );
 		halo_exchange( L, z, -1 );
-		symmetric_enqueue( L, z, r, sweeps );
+		{
+			Span timed( L->ctx, &L->stats.smoother_ns );
+			symmetric_enqueue( L, z, r, sweeps );
+		}
 		L->stats.nnz_visited += 2 * sweeps * L->nnz;
 	}
 
@@ -314,7 +388,10 @@ namespace slabgpu {
 		if( !L->R ) {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "restrict_vector: the coarsest level has no restriction operator" );
 		}
-		op_mxv( out, nullptr, L->R.get(), v_fine, SLAB_DESC_NONE );
+		{
+			Span timed( L->ctx, &L->stats.transfer_ns ); // multigrid.hpp:50-52
+			op_mxv( out, nullptr, L->R.get(), v_fine, SLAB_DESC_NONE );
+		}
 		L->stats.nnz_visited += L->R->nnz;
 	}
 
@@ -325,12 +402,15 @@ namespace slabgpu {
 		if( z_c->n != L->R->nrows || z->n != L->n ) {
 			fail( SLAB_ERR_DIMENSION_MISMATCH, "mxv: operand sizes do not match the matrix" );
 		}
-		if( L->ctx->fused_transfers ) {
-			// injected rows are the colour-0 block: position p <-> coarse index p
-			kern::prolong_add( L->ctx->stream, L->d_rows, static_cast< int64_t >( z_c->n ), z->d, z_c->d );
-		} else {
-			op_mxv( L->f.get(), nullptr, L->R.get(), z_c, SLAB_DESC_TRANSPOSE );
-			op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+		{
+			Span timed( L->ctx, &L->stats.transfer_ns ); // multigrid.hpp:75-78
+			if( L->ctx->fused_transfers ) {
+				// injected rows are the colour-0 block: position p <-> coarse index p
+				kern::prolong_add( L->ctx->stream, L->d_rows, static_cast< int64_t >( z_c->n ), z->d, z_c->d );
+			} else {
+				op_mxv( L->f.get(), nullptr, L->R.get(), z_c, SLAB_DESC_TRANSPOSE );
+				op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+			}
 		}
 		L->stats.nnz_visited += L->R->nnz;
 	}
@@ -493,6 +573,51 @@ namespace slabgpu {
 	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
 	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats ) {
 		slab_ctx_s * ctx = L->ctx;
+		if( ctx->profiling ) {
+			// the reference's instrumentation (multigrid.hpp:92-114, smoother.hpp:79-98): per-level V-cycle
+			// time with the coarser levels subtracted, smoother and transfer time inside it. Launch by
+			// launch, transfers as their own kernels so that they can be attributed.
+			Span whole( ctx, &L->stats.mg_ns );
+			{
+				Span smooth( ctx, &L->stats.smoother_ns );
+				symmetric_enqueue( L, z, r, sweeps );
+			}
+			if( L->coarser ) {
+				if( ctx->fused_transfers && L->is_stencil ) {
+					Span transfer( ctx, &L->stats.transfer_ns ); // residual + restriction in one kernel
+					kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+						static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d, nullptr );
+				} else {
+					op_mxv( L->f.get(), nullptr, L->A.get(), z, SLAB_DESC_NONE );
+					op_waxpby( L->f.get(), 1.0, r, -1.0, L->f.get() );
+					Span transfer( ctx, &L->stats.transfer_ns );
+					op_mxv( L->r_c.get(), nullptr, L->R.get(), L->f.get(), SLAB_DESC_NONE );
+				}
+				op_set_all( L->z_c.get(), 0.0 );
+				{
+					Span child( ctx, &L->stats.mg_ns, -1 ); // per-level time excludes the coarser levels
+					mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
+				}
+				{
+					Span transfer( ctx, &L->stats.transfer_ns );
+					if( ctx->fused_transfers && L->is_stencil ) {
+						kern::prolong_add( ctx->stream, L->d_rows, static_cast< int64_t >( L->z_c->n ), z->d, L->z_c->d );
+					} else {
+						op_mxv( L->f.get(), nullptr, L->R.get(), L->z_c.get(), SLAB_DESC_TRANSPOSE );
+						op_waxpby( z, 1.0, z, 1.0, L->f.get() );
+					}
+				}
+				if( L->plan != nullptr ) {
+					halo_exchange( L, z, 0 ); // the separate prolongation changed colour-0 boundary values
+				}
+				Span smooth( ctx, &L->stats.smoother_ns );
+				symmetric_enqueue( L, z, r, sweeps );
+			}
+			if( count_stats ) {
+				L->stats.nnz_visited += L->coarser ? 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz : 2 * sweeps * L->nnz;
+			}
+			return;
+		}
 		if( use_persistent( L, sweeps ) ) {
 			if( L->d_phases == nullptr || L->phases_z != z->d || L->phases_r != r->d || L->phases_sweeps != sweeps ) {
 				fail( SLAB_ERR_INTERNAL, "persistent V-cycle used without mg_vcycle_prepare" );
@@ -567,7 +692,7 @@ namespace slabgpu {
 		}
 		slab_ctx_s * ctx = L->ctx;
 		mg_vcycle_prepare( L, z, r, sweeps ); // allocations and uploads happen before any capture
-		if( !ctx->use_graphs ) {
+		if( !ctx->use_graphs || ctx->profiling ) {
 			halo_exchange( L, z, -1 ); // the caller's z: ghost copies may be stale
 			mg_vcycle_enqueue( L, z, r, sweeps, true );
 			return;

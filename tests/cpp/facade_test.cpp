@@ -112,6 +112,15 @@ int main() {
 		CHECK_THROWS_AS( cg_solve( ctx, neg, b, x0, plain ), SolverBreakdown );
 	}
 
+	{ // symmetry test passes on a generated hierarchy (test_bench.cpp:55-62)
+		ProblemLevel hierarchy = build_hierarchy( ctx, { 8, 8, 8 }, 3 );
+		const SymmetryReport verdict = symmetry_test( ctx, hierarchy, 123 );
+		CHECK( verdict.matrix_pass );
+		CHECK( verdict.precond_pass );
+		CHECK( verdict.tolerance > 0.0 );
+		CHECK( !verdict.skipped );
+	}
+
 	std::printf( failures == 0 ? "facade_test: all checks passed\n" : "facade_test: %d failure(s)\n", failures );
 	return failures == 0 ? 0 : 1;
 }
