@@ -69,7 +69,9 @@ uint64_t slab_launch_count( void );
 /* chain kernels with programmatic dependent launch (griddepcontrol): 1 (default) or 0. Process-wide. */
 int slab_set_programmatic_launch( int enabled );
 /* performance knobs that never change results: "stream_rows" (launches with at least this many rows
- * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl". Process-wide. */
+ * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl", "halo_overlap" (boundary
+ * rows first, halo messages beside the interior rows), "persist_rows" / "persist_blocks_per_sm" (persistent
+ * coarse-level kernel), "l2_window". Process-wide; each also has an environment variable SLAB_<KEY>. */
 int slab_set_tuning( const char * key, int64_t value );
 
 /* ------------------------------------------------------------------ context */

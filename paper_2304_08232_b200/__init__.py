@@ -6,4 +6,4 @@ The product is the CUDA shared library ``libslab_b200.so`` (hand-written kernels
 operator API for Python callers; nothing here computes on the CPU.
 """
 from ._capi import *  # noqa: F401,F403
-from ._capi import LIB_PATH, SIGNATURES, load_library, launch_count, set_programmatic_launch  # noqa: F401
+from ._capi import LIB_PATH, SIGNATURES, load_library, launch_count, set_programmatic_launch, set_tuning  # noqa: F401

@@ -89,6 +89,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_use_pdl = value ? 1 : 0;
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
+		} else if( k == "halo_overlap" ) {
+			g_halo_overlap = value ? 1 : 0;
 		} else if( k == "l2_window" ) {
 			g_l2_window = static_cast< int >( value );
 		} else if( k == "persist_debug" ) {
@@ -217,6 +219,9 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_PERSIST_BLOCKS_PER_SM" ) ) {
 			g_persist_blocks_per_sm = std::atoi( v );
+		}
+		if( const char * v = std::getenv( "SLAB_HALO_OVERLAP" ) ) {
+			g_halo_overlap = std::atoi( v ) ? 1 : 0;
 		}
 		if( const char * v = std::getenv( "SLAB_L2_WINDOW" ) ) {
 			g_l2_window = std::atoi( v );

@@ -252,7 +252,18 @@ namespace slabgpu {
 	// bring the ghost copies of v up to date: colour < 0 exchanges every colour. No-op on
 	// single-process contexts and in manual-exchange mode (no communicator attached).
 	void halo_exchange( slab_level_s * L, slab_vec_s * v, int color );
-	void halo_exchange_plan( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color );
+	void halo_exchange_plan( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color, cudaStream_t stream = nullptr );
+	// boundary rows of every colour as colour-major positions (level.cu computes them, the plan owns them)
+	void halo_plan_set_boundary( slab_ctx_s * ctx, HaloPlan * plan, const std::vector< std::vector< int32_t > > & per_color,
+		int64_t npos );
+	bool halo_overlap_active( const slab_ctx_s * ctx, const HaloPlan * plan ); // split colour steps into boundary + interior?
+	bool halo_has_comm( const slab_ctx_s * ctx );
+	void halo_fork( slab_ctx_s * ctx );  // comm stream waits for what the main stream has enqueued so far
+	void halo_join( slab_ctx_s * ctx );  // main stream waits for what the comm stream has enqueued so far
+	cudaStream_t halo_comm_stream( slab_ctx_s * ctx );
+	const int32_t * halo_boundary_positions( const HaloPlan * plan, int color, int64_t * count );
+	const uint8_t * halo_boundary_flags( const HaloPlan * plan );
+	extern int g_halo_overlap;
 	void allreduce_slot( slab_ctx_s * ctx, int slot ); // sum d_scalars[slot] over ranks, in place
 	void dist_destroy( slab_ctx_s * ctx );
 

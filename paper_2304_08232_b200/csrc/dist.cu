@@ -120,6 +120,11 @@ namespace slabgpu {
 		if( ctx->dist->comm != nullptr ) {
 			nccl().CommDestroy( ctx->dist->comm );
 		}
+		if( ctx->dist->comm_stream != nullptr ) {
+			cudaStreamDestroy( ctx->dist->comm_stream );
+			cudaEventDestroy( ctx->dist->ev_boundary );
+			cudaEventDestroy( ctx->dist->ev_arrived );
+		}
 		delete ctx->dist;
 		ctx->dist = nullptr;
 	}
@@ -201,10 +206,73 @@ namespace slabgpu {
 		return plan.release();
 	}
 
+	int g_halo_overlap = 1; // compute boundary rows first and overlap their messages with the interior rows
+
+	void halo_plan_set_boundary( slab_ctx_s * ctx, HaloPlan * plan, const std::vector< std::vector< int32_t > > & per_color,
+		int64_t npos ) {
+		std::vector< int32_t > all;
+		std::vector< uint8_t > flags( static_cast< size_t >( npos > 0 ? npos : 1 ), 0 );
+		for( int c = 0; c < 8; ++c ) {
+			plan->bnd_off[ c ] = static_cast< int64_t >( all.size() );
+			if( c < static_cast< int >( per_color.size() ) ) {
+				for( const int32_t pos : per_color[ c ] ) {
+					all.push_back( pos );
+					flags[ pos ] = 1;
+				}
+			}
+		}
+		plan->bnd_off[ 8 ] = static_cast< int64_t >( all.size() );
+		SLAB_CUDA( cudaMalloc( &plan->d_bnd_pos, std::max< size_t >( all.size(), 1 ) * sizeof( int32_t ) ) );
+		SLAB_CUDA( cudaMalloc( &plan->d_is_bnd, flags.size() ) );
+		upload_sync( ctx->stream, plan->d_bnd_pos, all.data(), all.size() * sizeof( int32_t ) );
+		upload_sync( ctx->stream, plan->d_is_bnd, flags.data(), flags.size() );
+	}
+
+	bool halo_overlap_active( const slab_ctx_s * ctx, const HaloPlan * plan ) {
+		return g_halo_overlap && ctx->dist != nullptr && plan != nullptr && plan->D.n_ghost > 0 && plan->d_is_bnd != nullptr;
+	}
+
+	bool halo_has_comm( const slab_ctx_s * ctx ) {
+		return ctx->dist != nullptr && ctx->dist->comm != nullptr;
+	}
+
+	cudaStream_t halo_comm_stream( slab_ctx_s * ctx ) {
+		DistState * d = ctx->dist;
+		if( d->comm_stream == nullptr ) {
+			SLAB_CUDA( cudaStreamCreateWithFlags( &d->comm_stream, cudaStreamNonBlocking ) );
+			SLAB_CUDA( cudaEventCreateWithFlags( &d->ev_boundary, cudaEventDisableTiming ) );
+			SLAB_CUDA( cudaEventCreateWithFlags( &d->ev_arrived, cudaEventDisableTiming ) );
+		}
+		return d->comm_stream;
+	}
+
+	void halo_fork( slab_ctx_s * ctx ) {
+		cudaStream_t comm = halo_comm_stream( ctx );
+		SLAB_CUDA( cudaEventRecord( ctx->dist->ev_boundary, ctx->stream ) );
+		SLAB_CUDA( cudaStreamWaitEvent( comm, ctx->dist->ev_boundary, 0 ) );
+	}
+
+	void halo_join( slab_ctx_s * ctx ) {
+		cudaStream_t comm = halo_comm_stream( ctx );
+		SLAB_CUDA( cudaEventRecord( ctx->dist->ev_arrived, comm ) );
+		SLAB_CUDA( cudaStreamWaitEvent( ctx->stream, ctx->dist->ev_arrived, 0 ) );
+	}
+
+	const int32_t * halo_boundary_positions( const HaloPlan * plan, int color, int64_t * count ) {
+		*count = plan->bnd_off[ color + 1 ] - plan->bnd_off[ color ];
+		return plan->d_bnd_pos + plan->bnd_off[ color ];
+	}
+
+	const uint8_t * halo_boundary_flags( const HaloPlan * plan ) {
+		return plan->d_is_bnd;
+	}
+
 	void halo_plan_destroy( HaloPlan * plan ) {
 		if( plan == nullptr ) {
 			return;
 		}
+		cudaFree( plan->d_bnd_pos );
+		cudaFree( plan->d_is_bnd );
 		cudaFree( plan->d_send_src );
 		cudaFree( plan->d_sendbuf );
 		for( int c = 0; c < 8; ++c ) {
@@ -215,16 +283,21 @@ namespace slabgpu {
 	}
 
 	// pack the boundary values of v (one colour, or all) into the plan's send buffer
-	void halo_pack( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color ) {
+	void halo_pack_on( cudaStream_t st, HaloPlan * plan, slab_vec_s * v, int color ) {
 		if( color < 0 ) {
-			kern::halo_pack( ctx->stream, plan->d_send_src, nullptr, plan->total_send, v->d, plan->d_sendbuf );
+			kern::halo_pack( st, plan->d_send_src, nullptr, plan->total_send, v->d, plan->d_sendbuf );
 		} else {
-			kern::halo_pack( ctx->stream, plan->d_color_src[ color ], plan->d_color_dst[ color ], plan->color_count[ color ],
-				v->d, plan->d_sendbuf );
+			kern::halo_pack( st, plan->d_color_src[ color ], plan->d_color_dst[ color ], plan->color_count[ color ], v->d,
+				plan->d_sendbuf );
 		}
 	}
 
-	void halo_exchange_plan( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color ) {
+	void halo_pack( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color ) {
+		halo_pack_on( ctx->stream, plan, v, color );
+	}
+
+	void halo_exchange_plan( slab_ctx_s * ctx, HaloPlan * plan, slab_vec_s * v, int color, cudaStream_t stream ) {
+		cudaStream_t st = stream != nullptr ? stream : ctx->stream;
 		if( plan == nullptr || ctx->dist == nullptr || ctx->dist->comm == nullptr || plan->D.n_ghost == 0 ) {
 			return; // single process, or manual-exchange mode (tests drive pack/unpack themselves)
 		}
@@ -232,7 +305,7 @@ namespace slabgpu {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "vector has no room for the ghost points of this level "
 				"(create vectors after the hierarchy on a distributed context)" );
 		}
-		halo_pack( ctx, plan, v, color );
+		halo_pack_on( st, plan, v, color );
 		NcclApi & api = nccl();
 		void * comm = ctx->dist->comm;
 		nccl_check( api.GroupStart(), "ncclGroupStart" );
@@ -250,11 +323,11 @@ namespace slabgpu {
 			}
 			if( send_n > 0 ) {
 				nccl_check( api.Send( plan->d_sendbuf + plan->send_off[ dir ][ c0 ], static_cast< size_t >( send_n ),
-					kNcclFloat64, peer, comm, ctx->stream ), "ncclSend" );
+					kNcclFloat64, peer, comm, st ), "ncclSend" );
 			}
 			if( recv_n > 0 ) {
 				nccl_check( api.Recv( v->d + plan->D.n_local + plan->D.ghost_base[ dir ][ c0 ], static_cast< size_t >( recv_n ),
-					kNcclFloat64, peer, comm, ctx->stream ), "ncclRecv" );
+					kNcclFloat64, peer, comm, st ), "ncclRecv" );
 			}
 		}
 		nccl_check( api.GroupEnd(), "ncclGroupEnd" );

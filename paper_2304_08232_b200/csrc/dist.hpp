@@ -22,6 +22,9 @@ namespace slabgpu {
 		void * comm = nullptr;    // ncclComm_t; null = manual-exchange mode
 		uint64_t ghost_capacity = 0; // largest ghost count over the levels built so far
 		uint64_t exchanges = 0;   // halo exchanges enqueued (diagnostics)
+		cudaStream_t comm_stream = nullptr; // halo messages of a colour step travel here, beside the interior rows
+		cudaEvent_t ev_boundary = nullptr;  // main stream: boundary rows done
+		cudaEvent_t ev_arrived = nullptr;   // comm stream: ghosts of the colour arrived
 	};
 
 	struct HaloPlan {
@@ -35,6 +38,12 @@ namespace slabgpu {
 		int32_t * d_color_src[ 8 ] = { nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr };
 		int32_t * d_color_dst[ 8 ] = { nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr };
 		int64_t color_count[ 8 ] = { 0, 0, 0, 0, 0, 0, 0, 0 };
+		// boundary rows (= rows some neighbour holds a ghost copy of) as positions of the colour-major
+		// row order, per colour, ascending; and a flag per position. They let a colour step compute its
+		// boundary rows first and overlap their halo messages with the interior rows.
+		int32_t * d_bnd_pos = nullptr;
+		int64_t bnd_off[ 9 ] = { 0, 0, 0, 0, 0, 0, 0, 0, 0 };
+		uint8_t * d_is_bnd = nullptr;
 	};
 
 	inline void rank_coords( const int p[ 3 ], int rank, int r[ 3 ] ) {

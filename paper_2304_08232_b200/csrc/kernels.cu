@@ -404,15 +404,21 @@ namespace slabgpu {
 			__global__ void __launch_bounds__( kBlock, 2 ) k_gs_color( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
-				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
+				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
+				// pos_list: the launch covers exactly these positions (the boundary rows of a colour, computed
+				// first so that their halo messages travel while the interior rows run); skip: positions
+				// flagged here are left out (the interior launch of the same colour)
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				int32_t i = -1;
 				int64_t begin = 0;
+				int64_t coarse = 0;
 				int width = 0;
 				RowChunk rc;
 				if( k < pos_count ) {
-					const int64_t pos = pos_begin + k;
-					i = rows[ pos ];
+					const int64_t pos = pos_list != nullptr ? pos_list[ k ] : pos_begin + k;
+					coarse = pos - pos_begin;
+					i = skip != nullptr && skip[ pos ] ? -1 : rows[ pos ];
 					const int64_t s = pos >> 5;
 					const int64_t b = slice_off[ s ];
 					width = static_cast< int >( ( slice_off[ s + 1 ] - b ) >> 5 );
@@ -427,7 +433,7 @@ namespace slabgpu {
 				const double ri = r[ i ];
 				double zi = z[ i ];
 				if( flags & 1 ) {
-					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ k ] ) );
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ coarse ] ) );
 					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 					z[ i ] = zi;
 				}
@@ -440,8 +446,8 @@ namespace slabgpu {
 					double az = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, z, 0.0, -1, unused );
 					az = row_tail< false >( vals, cols, begin, width, z, az, -1, unused );
 					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
-					out[ k ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
-					zero[ k ] = 0.0;
+					out[ coarse ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+					zero[ coarse ] = 0.0;
 				}
 			}
 
@@ -541,21 +547,24 @@ namespace slabgpu {
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_batched( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r,
-				const double * __restrict__ src ) {
+				const double * __restrict__ src, const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( k >= pos_count ) {
 					return;
 				}
-				const int64_t pos = pos_begin + k;
+				const int64_t pos = pos_list != nullptr ? pos_list[ k ] : pos_begin + k; // see k_gs_color
+				if( skip != nullptr && skip[ pos ] ) {
+					return;
+				}
 				const int32_t i = rows[ pos ];
 				if( i < 0 ) {
 					return;
 				}
 				double zi = z[ i ];
 				if( src != nullptr ) { // prolongation fused in front, see k_gs_color
-					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ k ] ) );
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ pos - pos_begin ] ) );
 					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 					z[ i ] = zi;
 				}
@@ -1074,7 +1083,8 @@ namespace slabgpu {
 
 		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
 			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
-			const double * src, double * out, double * zero, size_t window_bytes ) {
+			const double * src, double * out, double * zero, size_t window_bytes, const int32_t * pos_list,
+			const uint8_t * skip ) {
 			if( pos_count == 0 ) {
 				return;
 			}
@@ -1090,27 +1100,27 @@ namespace slabgpu {
 				}
 				switch( g_stream_variant ) {
 					case 1:
-						launch( k_gs_color_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
+						launch( k_gs_color_batched< 9, 4 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong, pos_list, skip );
 						break;
 					case 3:
-						launch( k_gs_color_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
+						launch( k_gs_color_batched< 14, 3 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong, pos_list, skip );
 						break;
 					case 4:
-						launch( k_gs_color_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
+						launch( k_gs_color_batched< 5, 6 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong, pos_list, skip );
 						break;
 					case 5:
-						launch( k_gs_color_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
+						launch( k_gs_color_batched< 7, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong, pos_list, skip );
 						break;
 					case 6:
-						launch( k_gs_color, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, flags, src, out, zero );
+						launch( k_gs_color, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, flags, src, out, zero, pos_list, skip );
 						break;
 					default:
-						launch( k_gs_color_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong );
+						launch( k_gs_color_batched< 9, 5 >, grid, kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z, r, prolong, pos_list, skip );
 				}
 				return;
 			}
 			launch( k_gs_color, blocks_for( pos_count ), kBlock, st, slice_off, vals, cols, rows, pos_begin, pos_count, z,
-				r, flags, src, out, zero );
+				r, flags, src, out, zero, pos_list, skip );
 		}
 
 		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,

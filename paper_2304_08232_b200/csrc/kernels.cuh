@@ -38,7 +38,9 @@ namespace slabgpu {
 		// gs_color_step_can_fuse_residual(pos_count); both only on colour-0 steps of stencil levels.
 		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
 			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags = 0,
-			const double * src = nullptr, double * out = nullptr, double * zero = nullptr, size_t window_bytes = 0 );
+			const double * src = nullptr, double * out = nullptr, double * zero = nullptr, size_t window_bytes = 0,
+			const int32_t * pos_list = nullptr, const uint8_t * skip = nullptr );
+		// pos_list: cover exactly these positions (pos_count = their number); skip: leave flagged positions out
 		// window_bytes > 0: size of z; many-wave launches then ask the L2 to keep z in its persisting carve-out
 		bool gs_color_step_can_fuse_residual( int64_t pos_count );
 

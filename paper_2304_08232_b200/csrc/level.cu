@@ -4,6 +4,7 @@
 #include <limits>
 
 #include "common.hpp"
+#include "dist.hpp"
 #include "kernels.cuh"
 
 slab_level_s::~slab_level_s() {
@@ -144,6 +145,35 @@ namespace slabgpu {
 				L->color_pos[ k + 1 ] = L->color_pos[ k ] + round_up( static_cast< int64_t >( size ), kSlice );
 			}
 			const int64_t npos = L->color_pos[ 8 ];
+			if( L->plan != nullptr && D.n_ghost > 0 ) {
+				// boundary rows of every colour, as positions of the colour-major order
+				std::vector< std::vector< int32_t > > boundary( 8 );
+				for( int c = 0; c < 8; ++c ) {
+					const int cc[ 3 ] = { c & 1, ( c >> 1 ) & 1, ( c >> 2 ) & 1 };
+					const int sx = count_parity( D.o[ 0 ], D.l[ 0 ], cc[ 0 ] ), sy = count_parity( D.o[ 1 ], D.l[ 1 ], cc[ 1 ] );
+					std::vector< int32_t > positions;
+					for( int dir = 0; dir < 27; ++dir ) {
+						if( dir == 13 || D.ghost_count[ dir ][ 0 ] + D.ghost_count[ dir ][ 1 ] + D.ghost_count[ dir ][ 2 ]
+								+ D.ghost_count[ dir ][ 3 ] + D.ghost_count[ dir ][ 4 ] + D.ghost_count[ dir ][ 5 ] + D.ghost_count[ dir ][ 6 ]
+								+ D.ghost_count[ dir ][ 7 ] == 0 ) {
+							continue; // no neighbour in that direction
+						}
+						std::vector< int32_t > list;
+						send_list( D, dir, c, list );
+						for( const int32_t idx : list ) {
+							const int ix = idx % D.l[ 0 ], iy = ( idx / D.l[ 0 ] ) % D.l[ 1 ], iz = idx / ( D.l[ 0 ] * D.l[ 1 ] );
+							const int qx = ( D.o[ 0 ] + ix - first_parity( D.o[ 0 ], cc[ 0 ] ) ) >> 1;
+							const int qy = ( D.o[ 1 ] + iy - first_parity( D.o[ 1 ], cc[ 1 ] ) ) >> 1;
+							const int qz = ( D.o[ 2 ] + iz - first_parity( D.o[ 2 ], cc[ 2 ] ) ) >> 1;
+							positions.push_back( static_cast< int32_t >( L->color_pos[ c ] + qx + static_cast< int64_t >( sx ) * ( qy + static_cast< int64_t >( sy ) * qz ) ) );
+						}
+					}
+					std::sort( positions.begin(), positions.end() );
+					positions.erase( std::unique( positions.begin(), positions.end() ), positions.end() );
+					boundary[ c ] = std::move( positions );
+				}
+				halo_plan_set_boundary( ctx, L->plan, boundary, npos );
+			}
 			SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< int64_t >( npos, 1 ) * sizeof( int32_t ) ) );
 			for( int k = 0; k < 8; ++k ) {
 				kern::color_rows( ctx->stream, D, k, L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ),
@@ -312,11 +342,38 @@ namespace slabgpu {
 		// entry; the step then sends the just-updated boundary values of colour k to the neighbours
 		// (only that colour moved), which restores the invariant for the next step.
 		void color_step_enqueue( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r, int flags = 0 ) {
-			kern::gs_color_step( L->ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
-				L->color_pos[ k ], static_cast< int64_t >( L->color_size[ k ] ), z->d, r->d, flags,
-				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr,
-				static_cast< size_t >( z->n_alloc ) * sizeof( double ) );
-			halo_exchange( L, z, static_cast< int >( k ) );
+			slab_ctx_s * ctx = L->ctx;
+			const double * src = ( flags & 1 ) ? L->z_c->d : nullptr;
+			double * out = ( flags & 2 ) ? L->r_c->d : nullptr;
+			double * zero = ( flags & 2 ) ? L->z_c->d : nullptr;
+			const size_t window = static_cast< size_t >( z->n_alloc ) * sizeof( double );
+			const int64_t count = static_cast< int64_t >( L->color_size[ k ] );
+			if( !halo_overlap_active( ctx, L->plan ) ) {
+				kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+					L->color_pos[ k ], count, z->d, r->d, flags, src, out, zero, window );
+				halo_exchange( L, z, static_cast< int >( k ) );
+				return;
+			}
+			// Distributed level: (1) the boundary rows of the colour, (2) their halo messages on the
+			// communication stream, (3) the interior rows on the main stream meanwhile, (4) join. Interior rows
+			// have no ghost neighbours and nobody reads the colour's ghost slots during this step, so the
+			// two streams touch disjoint data. Same arithmetic per row as the single launch.
+			int64_t nb = 0;
+			const int32_t * bpos = halo_boundary_positions( L->plan, static_cast< int >( k ), &nb );
+			if( nb > 0 ) {
+				kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+					L->color_pos[ k ], nb, z->d, r->d, flags, src, out, zero, 0, bpos, nullptr );
+			}
+			const bool comm = halo_has_comm( ctx );
+			if( comm ) {
+				halo_fork( ctx );
+				halo_exchange_plan( ctx, L->plan, z, static_cast< int >( k ), halo_comm_stream( ctx ) );
+			}
+			kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				L->color_pos[ k ], count, z->d, r->d, flags, src, out, zero, window, nullptr, halo_boundary_flags( L->plan ) );
+			if( comm ) {
+				halo_join( ctx );
+			}
 		}
 
 		void forward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:80-82

@@ -154,8 +154,19 @@ def test_distributed_spmv_and_sweeps_equal_global_bitwise(slab, ctx, grid, local
     assert np.array_equal(w.gather(lv, z), zg.values())
 
 
+@pytest.mark.parametrize("overlap", [1, 0])
 @pytest.mark.parametrize("grid,local,levels", GRIDS[:4])
-def test_distributed_vcycle_equals_global_bitwise(slab, ctx, grid, local, levels):
+def test_distributed_vcycle_equals_global_bitwise(slab, ctx, grid, local, levels, overlap):
+    """overlap=1: every colour step runs as boundary rows (position list) + interior rows (skip flags),
+    the shape whose halo messages overlap the interior on real ranks; overlap=0: one launch per step."""
+    slab.set_tuning("halo_overlap", overlap)
+    try:
+        _vcycle_case(slab, ctx, grid, local, levels)
+    finally:
+        slab.set_tuning("halo_overlap", 1)
+
+
+def _vcycle_case(slab, ctx, grid, local, levels):
     w = World(slab, grid, local, levels)
     n_global = int(np.prod(w.global_dims))
     single = ctx.build_hierarchy(w.global_dims, levels)
