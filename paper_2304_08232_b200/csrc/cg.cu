@@ -145,7 +145,7 @@ namespace slabgpu {
 		const uint64_t limit = already_converged ? 0 : planned;
 
 		// iteration graph, cached per (x, config)
-		const bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
+		bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
 			mg_vcycle_prepare( H, ws->z.get(), ws->r.get(), cfg->sweeps ); // before any capture
 		}
@@ -166,28 +166,46 @@ namespace slabgpu {
 					kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
 				cudaGraph_t graph = nullptr;
 				const uint64_t before = g_launch_count;
-				SLAB_CUDA( cudaStreamBeginCapture( st, cudaStreamCaptureModeThreadLocal ) );
+				bool captured = false;
 				try {
-					iteration_enqueue( H, ws, x, cfg );
-				} catch( ... ) {
-					cudaStreamEndCapture( st, &graph );
-					if( graph ) {
-						cudaGraphDestroy( graph );
+					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
+					try {
+						iteration_enqueue( H, ws, x, cfg );
+					} catch( ... ) {
+						cudaStreamEndCapture( st, &graph );
+						if( graph ) {
+							cudaGraphDestroy( graph );
+							graph = nullptr;
+						}
+						throw;
 					}
-					throw;
+					SLAB_CUDA( cudaStreamEndCapture( st, &graph ) );
+					ws->iter_launches = g_launch_count - before;
+					const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph, 0 );
+					cudaGraphDestroy( graph );
+					SLAB_CUDA( err );
+					captured = true;
+				} catch( const Error & ) {
+					// With a communicator attached the iteration contains NCCL operations on two streams; if
+					// this driver/NCCL pair refuses to capture them, this rank enqueues the same operations
+					// launch by launch instead (the traffic on the wire is identical, so ranks may differ).
+					if( !halo_has_comm( ctx ) ) {
+						throw;
+					}
+					cudaGetLastError();
+					ws->iter_exec = nullptr;
+					ctx->use_graphs = 0;
+					graphs = false;
 				}
-				SLAB_CUDA( cudaStreamEndCapture( st, &graph ) );
-				ws->iter_launches = g_launch_count - before;
 				g_launch_count = before;
-				const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph, 0 );
-				cudaGraphDestroy( graph );
-				SLAB_CUDA( err );
-				ws->key_x = x->d;
-				ws->key_sweeps = cfg->sweeps;
-				ws->key_precond = cfg->use_preconditioner;
-				ws->key_dot = ctx->dot_mode;
-				ws->key_fused = ctx->fused_transfers;
-				ws->key_epoch = g_tuning_epoch;
+				if( captured ) {
+					ws->key_x = x->d;
+					ws->key_sweeps = cfg->sweeps;
+					ws->key_precond = cfg->use_preconditioner;
+					ws->key_dot = ctx->dot_mode;
+					ws->key_fused = ctx->fused_transfers;
+					ws->key_epoch = g_tuning_epoch;
+				}
 			}
 		}
 

@@ -762,7 +762,7 @@ namespace slabgpu {
 			}
 			cudaGraph_t graph = nullptr;
 			const uint64_t launches_before = g_launch_count;
-			SLAB_CUDA( cudaStreamBeginCapture( ctx->stream, cudaStreamCaptureModeThreadLocal ) );
+			SLAB_CUDA( cudaStreamBeginCapture( ctx->stream, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 			try {
 				halo_exchange( L, z, -1 );
 				mg_vcycle_enqueue( L, z, r, sweeps, false );
