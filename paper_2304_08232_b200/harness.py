@@ -239,3 +239,72 @@ def report_from_json(text: str) -> Report:
     agg = Aggregate(doc["aggregate"]["mean_solve_seconds"], doc["aggregate"]["mg_share"],
                     [LevelShares(**l) for l in doc["aggregate"]["levels"]])
     return Report(cfg, doc["generation_seconds"], SymmetryReport(**doc["symmetry"]), runs, agg)
+
+
+# ---------------------------------------------------------------- report.hpp:270-360 (CSV projection)
+
+
+@dataclass
+class CsvRow:  # report.hpp:273-280; level is None for per-run summary rows
+    run: int = 0
+    level: Optional[int] = None
+    kernel: str = ""
+    value: float = 0.0
+
+
+def report_to_rows(report: Report) -> List[CsvRow]:
+    rows: List[CsvRow] = []
+    for run in report.runs:
+        for lt in run.levels:
+            rows.append(CsvRow(run.run, lt.level, "smoother_seconds", lt.smoother_seconds))
+            rows.append(CsvRow(run.run, lt.level, "transfer_seconds", lt.transfer_seconds))
+            rows.append(CsvRow(run.run, lt.level, "mg_seconds", lt.mg_seconds))
+            rows.append(CsvRow(run.run, lt.level, "nnz_visited", float(lt.nnz_visited)))
+        rows.append(CsvRow(run.run, None, "solve_seconds", run.solve_seconds))
+        rows.append(CsvRow(run.run, None, "iterations", float(run.iterations)))
+        rows.append(CsvRow(run.run, None, "final_residual", run.final_residual))
+        rows.append(CsvRow(run.run, None, "converged", 1.0 if run.converged else 0.0))
+    return rows
+
+
+def _double_to_string(v: float) -> str:
+    """text.hpp:28-33 — std::to_chars: the shortest decimal form that parses back identically."""
+    if v == int(v) and abs(v) < 1e15:
+        return str(int(v)) if v != 0 or math.copysign(1.0, v) > 0 else "-0"
+    text = repr(float(v))
+    if "e" in text:  # to_chars prints 1e-05 as 1e-05 too; both forms round-trip
+        mant, exp = text.split("e")
+        sign = "-" if exp.startswith("-") else "+"
+        digits = exp.lstrip("+-").rjust(2, "0")
+        return f"{mant}e{sign}{digits}"
+    return text
+
+
+def rows_to_csv(rows: List[CsvRow]) -> str:
+    out = ["run,level,kernel,value"]
+    for row in rows:
+        level = "" if row.level is None else str(row.level)
+        out.append(f"{row.run},{level},{row.kernel},{_double_to_string(row.value)}")
+    return "\n".join(out) + "\n"
+
+
+def csv_to_rows(text: str) -> List[CsvRow]:
+    lines = text.split("\n")
+    if not lines or lines[0] != "run,level,kernel,value":
+        raise slab.InvalidArgument("csv_to_rows: missing or unexpected header")
+    rows = []
+    for line in lines[1:]:
+        if not line:
+            continue
+        fields = line.split(",")
+        if len(fields) != 4:
+            raise slab.InvalidArgument(f"csv_to_rows: expected 4 fields, got line '{line}'")
+        try:
+            rows.append(CsvRow(int(fields[0]), None if fields[1] == "" else int(fields[1]), fields[2], float(fields[3])))
+        except ValueError as exc:
+            raise slab.InvalidArgument(f"csv_to_rows: cannot parse '{line}'") from exc
+    return rows
+
+
+def report_to_csv(report: Report) -> str:
+    return rows_to_csv(report_to_rows(report))

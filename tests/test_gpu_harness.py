@@ -143,6 +143,21 @@ def test_json_report_round_trips_and_has_the_reference_keys(slab, ctx, harness):
                                                           "mg_seconds", "nnz_visited"])
 
 
+def test_csv_projection_round_trips(slab, ctx, harness):
+    """test_bench.cpp:168-176, report.hpp:270-360"""
+    report = harness.run_benchmark(ctx, small_config(harness))
+    rows = harness.report_to_rows(report)
+    csv = harness.rows_to_csv(rows)
+    parsed = harness.csv_to_rows(csv)
+    assert parsed == rows and harness.rows_to_csv(parsed) == csv and harness.report_to_csv(report) == csv
+    assert csv.splitlines()[0] == "run,level,kernel,value"
+    assert len(rows) == 2 * (2 * 4 + 4)
+    with pytest.raises(slab.InvalidArgument):
+        harness.csv_to_rows("bad,header\n")
+    with pytest.raises(slab.InvalidArgument):
+        harness.csv_to_rows("run,level,kernel,value\n1,2,3\n")
+
+
 def test_configuration_invariants_and_symmetry_shapes(slab, ctx, harness):
     """test_bench.cpp:180-204"""
     failing = harness.SymmetryReport(matrix_pass=False, precond_pass=True)
