@@ -13,8 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libslab_b200.so")
-SOURCES = ["kernels.cu", "kernels_setup.cu", "containers.cu", "level.cu", "cg.cu", "dist.cu", "abi.cu"]
-HEADERS = ["common.hpp", "kernels.cuh", "decomp.hpp", "dist.hpp", os.path.join("..", "..", "include", "slab_b200.h")]
+SOURCES = ["kernels.cu", "kernels_setup.cu", "packed.cu", "containers.cu", "level.cu", "cg.cu", "dist.cu", "abi.cu"]
+HEADERS = ["common.hpp", "kernels.cuh", "device_util.cuh", "decomp.hpp", "dist.hpp", os.path.join("..", "..", "include", "slab_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,23 +42,51 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object (in parallel, only the stale ones) and link."""
     if not force and not needs_build():
         return LIB
-    sources = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB, *sources, "-lcudart", "-ldl"]
-    env = dict(os.environ)
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "_build")
+    os.makedirs(objdir, exist_ok=True)
+    nvcc = [_nvcc()]
     # /opt/gcc (the image's default CC) lacks some runtime pieces; nvcc works with the system g++
     if os.path.exists("/usr/bin/g++"):
-        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    proc = subprocess.run(cmd, capture_output=True, text=True, env=env)
-    if verbose or proc.returncode != 0:
-        sys.stderr.write(proc.stdout)
-        sys.stderr.write(proc.stderr)
-    if proc.returncode != 0:
+        nvcc += ["-ccbin", "/usr/bin/g++"]
+    headers = [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS]
+    newest_header = max(os.path.getmtime(h) for h in headers if os.path.exists(h))
+    sources = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+
+    def compile_one(name):
+        src = os.path.join(CSRC, name)
+        obj = os.path.join(objdir, name + ".o")
+        log = os.path.join(objdir, name + ".log")
+        stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_header)
+        if not stale:
+            return obj, 0, open(log).read() if os.path.exists(log) else ""
+        cmd = [*nvcc, *[f for f in NVCC_FLAGS if f != "-shared"], "-c", "-o", obj, src]
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        text = " ".join(cmd) + "\n" + proc.stdout + proc.stderr
+        with open(log, "w") as fh:
+            fh.write(text)
+        return obj, proc.returncode, text
+
+    with ThreadPoolExecutor(max_workers=min(8, len(sources))) as pool:
+        results = list(pool.map(compile_one, sources))
+    failed = [r for r in results if r[1] != 0]
+    if verbose or failed:
+        for _, _, text in (failed or results):
+            sys.stderr.write(text)
+    if failed:
         raise RuntimeError("nvcc failed building libslab_b200.so")
-    log = os.path.join(HERE, "build_ptxas.log")
-    with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+    link = [*nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *[r[0] for r in results],
+            "-lcudart", "-ldl"]
+    proc = subprocess.run(link, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stdout + proc.stderr)
+        raise RuntimeError("nvcc failed linking libslab_b200.so")
+    with open(os.path.join(HERE, "build_ptxas.log"), "w") as fh:
+        fh.write("\n".join(r[2] for r in results))
     return LIB
 
 

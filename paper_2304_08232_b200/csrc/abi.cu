@@ -87,6 +87,18 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_stream_variant = static_cast< int >( value );
 		} else if( k == "pdl" ) {
 			g_use_pdl = value ? 1 : 0;
+		} else if( k == "packed" ) {
+			g_use_packed = value ? 1 : 0;
+		} else if( k == "pack_build" ) {
+			g_pack_build = value ? 1 : 0;
+		} else if( k == "packed_block" ) {
+			g_packed_block = static_cast< int >( value );
+		} else if( k == "packed_batch" ) {
+			g_packed_batch = static_cast< int >( value );
+		} else if( k == "packed_deep_rows" ) {
+			g_packed_deep_rows = value;
+		} else if( k == "packed_min_rows" ) {
+			g_packed_min_rows = value;
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
 		} else if( k == "halo_overlap" ) {
@@ -138,14 +150,30 @@ int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, in
 		kern::proto_permute_cols( st, level->colorA.cols, nat2pos, entries, pcols );
 		kern::proto_gather_to_pos( st, level->d_rows, npos, z->d, zp );
 		kern::proto_gather_to_pos( st, level->d_rows, npos, r->d, rp );
-		const auto sweep = [ & ]() {
-			for( uint64_t k = 0; k < level->num_colors; ++k ) {
+		// position-space matrix: same slices and values, permuted columns; packed against row == position.
+		// Positions of padding rows never occur as columns, but rows must not read them: the row list marks them.
+		Sell PS = level->colorA;
+		PS.cols = pcols;
+		PS.packed = Packed();
+		if( g_use_packed ) {
+			sell_pack( ctx, PS, nullptr );
+		}
+		const bool packed = PS.packed.usable();
+		const auto step = [ & ]( uint64_t k ) {
+			if( packed ) {
+				kern::gs_color_step_packed( st, PS, nullptr, level->color_pos[ k ], static_cast< int64_t >( level->color_size[ k ] ),
+					zp, rp, 0, nullptr, nullptr, nullptr, nullptr, nullptr );
+			} else {
 				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k ],
 					static_cast< int64_t >( level->color_size[ k ] ), zp, rp );
 			}
+		};
+		const auto sweep = [ & ]() {
+			for( uint64_t k = 0; k < level->num_colors; ++k ) {
+				step( k );
+			}
 			for( uint64_t k = level->num_colors; k > 0; --k ) {
-				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k - 1 ],
-					static_cast< int64_t >( level->color_size[ k - 1 ] ), zp, rp );
+				step( k - 1 );
 			}
 		};
 		sweep(); // one sweep to compare
@@ -171,6 +199,11 @@ int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, in
 		float t = 0.0f;
 		SLAB_CUDA( cudaEventElapsedTime( &t, ctx->timer_start, ctx->timer_stop ) );
 		if( ms ) *ms = t / reps;
+		if( packed && max_diff ) {
+			std::fprintf( stderr, "position-space dictionary: %d entries, %lld escaped rows\n", PS.packed.dict_size,
+				static_cast< long long >( PS.packed.escaped_rows ) );
+		}
+		PS.packed.release();
 		cudaFree( nat2pos );
 		cudaFree( pcols );
 		cudaFree( zp );
@@ -213,6 +246,15 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_STREAM_VARIANT" ) ) {
 			g_stream_variant = std::atoi( v );
+		}
+		if( const char * v = std::getenv( "SLAB_PACKED" ) ) {
+			g_use_packed = std::atoi( v ) ? 1 : 0;
+		}
+		if( const char * v = std::getenv( "SLAB_PACK_BUILD" ) ) {
+			g_pack_build = std::atoi( v ) ? 1 : 0;
+		}
+		if( const char * v = std::getenv( "SLAB_PACKED_BLOCK" ) ) {
+			g_packed_block = std::atoi( v );
 		}
 		if( const char * v = std::getenv( "SLAB_PERSIST_ROWS" ) ) {
 			g_persist_rows = std::atoll( v );

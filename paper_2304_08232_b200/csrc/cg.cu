@@ -69,7 +69,7 @@ namespace slabgpu {
 				// tree-dot mode: p'Ap rides on the product's epilogue and r'r on the x/r update — two
 				// passes over the vectors and two launches fewer per iteration
 				halo_exchange( H, p, -1 );
-				kern::spmv( st, H->A->sell.slice_off, H->A->sell.vals, H->A->sell.cols, p->d, q->d,
+				kern::spmv( st, H->A->sell, p->d, q->d,
 					static_cast< int64_t >( H->n ), ctx->d_partials, ctx->d_counter, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
 				allreduce_slot( ctx, S_PQ );
 				kern::cg_update_xr_dot( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,

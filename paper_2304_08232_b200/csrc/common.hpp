@@ -63,6 +63,12 @@ namespace slabgpu {
 	extern int g_stream_variant;
 	extern uint64_t g_launch_count;
 	extern int g_use_pdl; // chain kernels with programmatic dependent launch (default on)
+	extern int g_use_packed;   // run products and colour steps from the dictionary-coded matrix copy when one exists
+	extern int g_pack_build;   // build the dictionary-coded copy when a matrix is created
+	extern int g_packed_block; // threads per block of the packed kernels (tuning)
+	extern int g_packed_batch;
+	extern int64_t g_packed_deep_rows;
+	extern int64_t g_packed_min_rows;
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
 	}
@@ -73,16 +79,47 @@ namespace slabgpu {
 	// device scalar slots used by the CG driver (doubles in ctx->d_scalars)
 	enum Scalar { S_RHO = 0, S_RHO_PREV, S_PQ, S_RR, S_TMP, S_BB, S_COUNT = 16 };
 
+	// Dictionary-coded companion of a SELL matrix (packed.cu). Every stored entry is replaced by one
+	// byte: the index of its (column - row, value) pair in a dictionary of at most 254 pairs found in
+	// the matrix itself. Code 0 is padding; a row whose first code is 255 has an entry outside the
+	// dictionary and is read from the plain SELL arrays instead. A row occupies `chunks` 16-byte words,
+	// slice-interleaved like the SELL arrays: word j of lane l of slice s at [(s*chunks + j)*32 + l].
+	// The last byte of a row's words holds the code of its diagonal entry (0 = none).
+	struct alignas( 16 ) DictEntry {
+		double val;
+		int32_t delta;
+		int32_t unused;
+	};
+	struct Packed {
+		int max_width = 0;         // widest row (stored entries)
+		int ncodes = 0;            // width class the kernels are instantiated for (>= max_width)
+		int chunks = 0;            // 16-byte words stored per row = (ncodes + 16) / 16
+		uint4 * codes = nullptr;   // device
+		DictEntry * dict = nullptr; // device, 256 entries, entry 0 = {0.0, 0} (read by the encoder)
+		DictEntry * h_dict = nullptr; // host copy: the kernels take the dictionary as a launch parameter
+		int dict_size = 0;         // entries in use, including entry 0
+		int64_t escaped_rows = 0;  // rows that fall back to the plain arrays
+		void release();
+		bool usable() const {
+			return codes != nullptr;
+		}
+	};
+
 	struct Sell {
 		int64_t nrows = 0;     // logical rows (positions), multiple of kSlice not required
 		int64_t nslices = 0;
 		int64_t entries = 0;   // stored slots incl. padding
+		int max_width = 0;     // widest slice
+		Packed packed;         // optional, see sell_pack
 		int64_t * slice_off = nullptr; // device, nslices+1, in entries
 		double * vals = nullptr;       // device
 		int32_t * cols = nullptr;      // device, -1 = padding
 		void release();
 		uint64_t bytes() const {
 			return static_cast< uint64_t >( entries ) * 12u + static_cast< uint64_t >( nslices + 1 ) * 8u;
+		}
+		uint64_t packed_bytes() const {
+			return packed.usable() ? static_cast< uint64_t >( nslices ) * packed.chunks * kSlice * 16u + 256u * 16u : 0u;
 		}
 	};
 
@@ -242,6 +279,10 @@ namespace slabgpu {
 		const uint64_t * co, const double * va );
 	// SELL of the 27-point stencil over an arbitrary device row list (d_rows == nullptr: natural order)
 	Sell sell_stencil27( slab_ctx_s * ctx, const Decomp & D, const int32_t * d_rows, int64_t npos );
+	// packed.cu: build S.packed from the entries of S (d_rows: position -> row, nullptr = identity);
+	// leaves S.packed unusable when the matrix does not compress (rows wider than 64 entries, or
+	// too many rows with entries outside a 254-pair dictionary)
+	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows );
 	Decomp single_domain( uint64_t nx, uint64_t ny, uint64_t nz );
 
 	// ---- dist.cu (3D domain decomposition, halo exchange, allreduce)

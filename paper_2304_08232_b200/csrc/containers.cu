@@ -17,6 +17,7 @@ namespace slabgpu {
 		vals = nullptr;
 		cols = nullptr;
 		nrows = nslices = entries = 0;
+		packed.release();
 	}
 
 	// ---------------------------------------------------------------- scratch
@@ -91,6 +92,7 @@ namespace slabgpu {
 				off[ s + 1 ] = off[ s ] + static_cast< int64_t >( widths[ s ] ) * kSlice;
 			}
 			S.entries = off.back();
+			S.max_width = widths.empty() ? 0 : *std::max_element( widths.begin(), widths.end() );
 			SLAB_CUDA( cudaMalloc( &S.slice_off, off.size() * sizeof( int64_t ) ) );
 			SLAB_CUDA( cudaMalloc( &S.vals, std::max< int64_t >( S.entries, 1 ) * sizeof( double ) ) );
 			SLAB_CUDA( cudaMalloc( &S.cols, std::max< int64_t >( S.entries, 1 ) * sizeof( int32_t ) ) );
@@ -210,6 +212,7 @@ namespace slabgpu {
 		std::vector< int64_t > rows( nrows );
 		std::iota( rows.begin(), rows.end(), int64_t( 0 ) );
 		A->sell = sell_from_csr_rows( ctx, rows, ro, co, va );
+		sell_pack( ctx, A->sell, nullptr );
 		A->h_row_offsets.assign( ro, ro + nrows + 1 );
 		A->h_cols.assign( co, co + A->nnz );
 		A->h_vals.assign( va, va + A->nnz );
@@ -224,6 +227,7 @@ namespace slabgpu {
 		A->nrows = A->ncols = nx * ny * nz;
 		A->nnz = ( 3 * nx - 2 ) * ( 3 * ny - 2 ) * ( 3 * nz - 2 ); // problem.hpp:80-82
 		A->sell = sell_stencil27( ctx, single_domain( nx, ny, nz ), nullptr, static_cast< int64_t >( A->nrows ) );
+		sell_pack( ctx, A->sell, nullptr );
 		return A.release();
 	}
 
@@ -250,6 +254,7 @@ namespace slabgpu {
 		}
 		A->nnz = nnz; // equals (3nx-2)(3ny-2)(3nz-2) on a single domain (problem.hpp:80-82)
 		A->sell = sell_stencil27( ctx, D, nullptr, static_cast< int64_t >( A->nrows ) );
+		sell_pack( ctx, A->sell, nullptr );
 		return A.release();
 	}
 
@@ -412,9 +417,9 @@ namespace slabgpu {
 			halo_exchange_plan( A->ctx, A->plan, x, -1 ); // ghost copies of x before the gather
 		}
 		if( mask == nullptr ) {
-			kern::spmv( st, M->sell.slice_off, M->sell.vals, M->sell.cols, x->d, y->d, static_cast< int64_t >( M->nrows ) );
+			kern::spmv( st, M->sell, x->d, y->d, static_cast< int64_t >( M->nrows ) );
 		} else {
-			kern::spmv_masked( st, M->sell.slice_off, M->sell.vals, M->sell.cols, x->d, y->d, mask->d_members,
+			kern::spmv_masked( st, M->sell, x->d, y->d, mask->d_members,
 				static_cast< int64_t >( mask->count ) );
 		}
 	}

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "common.hpp"
+#include "device_util.cuh"
 
 namespace slabgpu {
 
@@ -51,12 +52,8 @@ namespace slabgpu {
 
 		namespace {
 
-			constexpr int kBlock = 256;
+			using namespace dev; // kBlock, blocks_for, dep_wait, dep_trigger, block_tree_sum
 			constexpr int kChunk = 27; // slots preloaded per row in one go (a full 27-point row)
-
-			inline unsigned int blocks_for( uint64_t count, int block = kBlock ) {
-				return static_cast< unsigned int >( ( count + block - 1 ) / block );
-			}
 
 			// Vector that the next launch should keep in the L2 persisting carve-out (the z of a fine-level
 			// colour step: every step gathers all of it while the matrix streams through). Consumed by the
@@ -96,15 +93,6 @@ namespace slabgpu {
 				cfg.numAttrs = count;
 				SLAB_CUDA( cudaLaunchKernelEx( &cfg, kernel, static_cast< KArgs >( args )... ) );
 				count_launch();
-			}
-
-			// wait until the previous kernel in the stream has completed and its writes are visible
-			__device__ __forceinline__ void dep_wait() {
-				asm volatile( "griddepcontrol.wait;" ::: "memory" );
-			}
-			// let the next kernel's blocks be scheduled as soon as SM resources free up
-			__device__ __forceinline__ void dep_trigger() {
-				asm volatile( "griddepcontrol.launch_dependents;" ::: "memory" );
 			}
 
 			// ------------------------------------------------------------ SELL row access
@@ -260,31 +248,8 @@ namespace slabgpu {
 				*out = 0.0;
 			}
 
-			// fixed-shape tree reduction: grid-stride partial per thread, shuffle tree per warp,
-			// shared-memory tree per block, last block folds the block partials the same way.
-			__device__ __forceinline__ double block_tree_sum( double v, double * smem ) {
-				#pragma unroll
-				for( int off = 16; off > 0; off >>= 1 ) {
-					v = __dadd_rn( v, __shfl_down_sync( 0xffffffffu, v, off ) );
-				}
-				const int warp = threadIdx.x >> 5;
-				const int lane = threadIdx.x & 31;
-				if( lane == 0 ) {
-					smem[ warp ] = v;
-				}
-				__syncthreads();
-				const int nwarps = blockDim.x >> 5;
-				v = threadIdx.x < nwarps ? smem[ threadIdx.x ] : 0.0;
-				if( warp == 0 ) {
-					#pragma unroll
-					for( int off = 16; off > 0; off >>= 1 ) {
-						v = __dadd_rn( v, __shfl_down_sync( 0xffffffffu, v, off ) );
-					}
-				}
-				__syncthreads();
-				return v; // valid in thread 0
-			}
-
+			// fixed-shape tree reduction: grid-stride partial per thread, block_tree_sum per block,
+			// last block folds the block partials the same way.
 			__device__ __forceinline__ void grid_tree_finish( double block_sum, double * partials, unsigned int * counter,
 				double * out, double * smem, bool * is_last ) {
 				if( threadIdx.x == 0 ) {
@@ -1022,18 +987,34 @@ namespace slabgpu {
 		}
 
 		uint64_t spmv_dot_blocks( int64_t nrows ) {
-			return blocks_for( nrows > 0 ? nrows : 1 );
+			return blocks_for( nrows > 0 ? nrows : 1, 128 ); // the smallest block any product kernel runs with
 		}
 
-		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, int64_t nrows, double * dot_partials, unsigned int * dot_counter,
-			double * dot_out ) {
+		void sum_partials( cudaStream_t st, const double * partials, uint64_t count, double * out ) {
+			launch( k_sum_partials, 1, 1024, st, partials, count, out );
+		}
+
+		namespace {
+			inline bool run_packed( const Sell & S, int64_t rows ) {
+				return g_use_packed && S.packed.usable() && rows >= g_packed_min_rows;
+			}
+		} // namespace
+
+		void spmv( cudaStream_t st, const Sell & S, const double * x, double * y, int64_t nrows, double * dot_partials,
+			unsigned int * dot_counter, double * dot_out ) {
 			if( nrows == 0 ) {
 				if( dot_out != nullptr ) {
 					launch( k_dot_empty, 1, 1, st, dot_out );
 				}
 				return;
 			}
+			if( run_packed( S, nrows ) ) {
+				spmv_packed( st, S, x, y, nullptr, nrows, dot_partials, dot_out );
+				return;
+			}
+			const int64_t * slice_off = S.slice_off;
+			const double * vals = S.vals;
+			const int32_t * cols = S.cols;
 			if( nrows >= g_stream_rows ) {
 				const unsigned int grid = blocks_for( nrows );
 				switch( g_stream_variant ) {
@@ -1068,26 +1049,40 @@ namespace slabgpu {
 			}
 		}
 
-		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, const int32_t * members, int64_t count ) {
+		void spmv_masked( cudaStream_t st, const Sell & S, const double * x, double * y, const int32_t * members,
+			int64_t count ) {
 			if( count == 0 ) {
 				return;
 			}
+			if( run_packed( S, count ) ) {
+				spmv_packed( st, S, x, y, members, count, nullptr, nullptr );
+				return;
+			}
+			const int64_t * slice_off = S.slice_off;
+			const double * vals = S.vals;
+			const int32_t * cols = S.cols;
 			launch( k_spmv< true >, blocks_for( count ), kBlock, st, slice_off, vals, cols, x, y, members, count,
 				static_cast< double * >( nullptr ), static_cast< unsigned int * >( nullptr ), static_cast< double * >( nullptr ) );
 		}
 
-		bool gs_color_step_can_fuse_residual( int64_t pos_count ) {
-			return pos_count < g_stream_rows; // the preload shape keeps the matrix row in registers
+		bool gs_color_step_can_fuse_residual( const Sell & S, int64_t pos_count ) {
+			// the packed and the preload shapes keep the matrix row in registers
+			return run_packed( S, pos_count ) || pos_count < g_stream_rows;
 		}
 
-		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
-			const double * src, double * out, double * zero, size_t window_bytes, const int32_t * pos_list,
-			const uint8_t * skip ) {
+		void gs_color_step( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t pos_begin, int64_t pos_count,
+			double * z, const double * r, int flags, const double * src, double * out, double * zero, size_t window_bytes,
+			const int32_t * pos_list, const uint8_t * skip ) {
 			if( pos_count == 0 ) {
 				return;
 			}
+			if( run_packed( S, pos_count ) ) {
+				gs_color_step_packed( st, S, rows, pos_begin, pos_count, z, r, flags, src, out, zero, pos_list, skip );
+				return;
+			}
+			const int64_t * slice_off = S.slice_off;
+			const double * vals = S.vals;
+			const int32_t * cols = S.cols;
 			if( pos_count >= g_stream_rows ) {
 				if( flags & 2 ) {
 					fail( SLAB_ERR_INTERNAL, "gs_color_step: the streaming shape cannot fuse the residual" );
@@ -1123,11 +1118,18 @@ namespace slabgpu {
 				r, flags, src, out, zero, pos_list, skip );
 		}
 
-		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c, double * zero ) {
+		void residual_restrict( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t n_coarse, const double * z,
+			const double * r, double * r_c, double * zero ) {
 			if( n_coarse == 0 ) {
 				return;
 			}
+			if( run_packed( S, n_coarse ) ) {
+				residual_restrict_packed( st, S, rows, n_coarse, z, r, r_c, zero );
+				return;
+			}
+			const int64_t * slice_off = S.slice_off;
+			const double * vals = S.vals;
+			const int32_t * cols = S.cols;
 			if( n_coarse >= g_stream_rows ) {
 				launch( k_residual_restrict_stream, blocks_for( n_coarse ), kBlock, st, slice_off, vals, cols, rows, n_coarse,
 					z, r, r_c, zero );

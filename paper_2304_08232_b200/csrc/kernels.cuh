@@ -8,6 +8,7 @@
 
 namespace slabgpu {
 	struct Decomp;
+	struct Sell;
 	namespace kern {
 
 		// ---- vector ops (operations.hpp:49-106)
@@ -25,32 +26,42 @@ namespace slabgpu {
 		// ---- SELL-32 matrix-vector products (operations.hpp:116-125, :164-174)
 		// dot_out != nullptr additionally reduces x'(A x) in the tree-dot shape (cg.hpp:122-123 in one pass);
 		// dot_partials then needs spmv_dot_blocks(nrows) doubles
-		void spmv( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, int64_t nrows, double * dot_partials = nullptr,
-			unsigned int * dot_counter = nullptr, double * dot_out = nullptr );
+		// Every matrix entry point takes the SELL and runs from its dictionary-coded copy (packed.cu) when
+		// one exists and g_use_packed is set; the arithmetic and its order are the same either way.
+		void spmv( cudaStream_t st, const Sell & S, const double * x, double * y, int64_t nrows,
+			double * dot_partials = nullptr, unsigned int * dot_counter = nullptr, double * dot_out = nullptr );
 		uint64_t spmv_dot_blocks( int64_t nrows );
-		void spmv_masked( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const double * x, double * y, const int32_t * members, int64_t count );
+		void spmv_masked( cudaStream_t st, const Sell & S, const double * x, double * y, const int32_t * members,
+			int64_t count );
+		// out = fold of `count` block partials in a fixed order
+		void sum_partials( cudaStream_t st, const double * partials, uint64_t count, double * out );
 
 		// ---- fused Gauss-Seidel colour step (smoother.hpp:60-72) on the colour-major SELL
 		// flags bit 0: prolongation fused in front (z[i] += src[k], multigrid.hpp:71-81); bit 1: residual +
 		// restriction fused behind (out[k], zero[k] = 0; multigrid.hpp:100-104) — only where
 		// gs_color_step_can_fuse_residual(pos_count); both only on colour-0 steps of stencil levels.
-		void gs_color_step( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags = 0,
+		void gs_color_step( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags = 0,
 			const double * src = nullptr, double * out = nullptr, double * zero = nullptr, size_t window_bytes = 0,
 			const int32_t * pos_list = nullptr, const uint8_t * skip = nullptr );
 		// pos_list: cover exactly these positions (pos_count = their number); skip: leave flagged positions out
 		// window_bytes > 0: size of z; many-wave launches then ask the L2 to keep z in its persisting carve-out
-		bool gs_color_step_can_fuse_residual( int64_t pos_count );
+		bool gs_color_step_can_fuse_residual( const Sell & S, int64_t pos_count );
 
 		// ---- fused grid transfers (multigrid.hpp:100-104 and :71-81)
 		// r_c[p] = 0 + 1*( 1*r[i] + (-1)*(A z)[i] ),  i = rows[p], p in the colour-0 block = injected rows
-		void residual_restrict( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * cols,
-			const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c,
+		void residual_restrict( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t n_coarse, const double * z, const double * r, double * r_c,
 			double * zero = nullptr ); // zero: the coarse guess, cleared by the same threads (multigrid.hpp:104)
 		// z[i] = 1*z[i] + 1*(0 + 1*z_c[p]) at the injected rows
 		void prolong_add( cudaStream_t st, const int32_t * rows, int64_t n_coarse, double * z, const double * z_c );
+
+		// ---- the same entry points on the dictionary-coded copy (packed.cu); S.packed must be usable
+		void spmv_packed( cudaStream_t st, const Sell & S, const double * x, double * y, const int32_t * members,
+			int64_t count, double * dot_partials, double * dot_out );
+		void gs_color_step_packed( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t pos_begin,
+			int64_t pos_count, double * z, const double * r, int flags, const double * src, double * out, double * zero,
+			const int32_t * pos_list, const uint8_t * skip );
+		void residual_restrict_packed( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t n_coarse,
+			const double * z, const double * r, double * r_c, double * zero );
 
 		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
 		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a

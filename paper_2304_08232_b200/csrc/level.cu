@@ -180,6 +180,7 @@ namespace slabgpu {
 					L->color_pos[ k + 1 ] - L->color_pos[ k ], L->d_rows );
 			}
 			L->colorA = sell_stencil27( ctx, D, L->d_rows, npos );
+		sell_pack( ctx, L->colorA, L->d_rows );
 			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
 			uint64_t n_coarse = 0;
 			if( with_restriction ) {
@@ -323,6 +324,7 @@ namespace slabgpu {
 		std::vector< int32_t > rows32( rows.begin(), rows.end() );
 		SLAB_CUDA( cudaMalloc( &L->d_rows, std::max< size_t >( rows32.size(), 1 ) * sizeof( int32_t ) ) );
 		upload_sync( ctx->stream, L->d_rows, rows32.data(), rows32.size() * sizeof( int32_t ) );
+		sell_pack( ctx, L->colorA, L->d_rows );
 		L->a_diag.reset( vec_new( ctx, n, 0.0 ) );
 		upload_sync( ctx->stream, L->a_diag->d, diag.data(), n * sizeof( double ) );
 		alloc_scratch( L.get(), 0 );
@@ -349,7 +351,7 @@ namespace slabgpu {
 			const size_t window = static_cast< size_t >( z->n_alloc ) * sizeof( double );
 			const int64_t count = static_cast< int64_t >( L->color_size[ k ] );
 			if( !halo_overlap_active( ctx, L->plan ) ) {
-				kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				kern::gs_color_step( ctx->stream, L->colorA, L->d_rows,
 					L->color_pos[ k ], count, z->d, r->d, flags, src, out, zero, window );
 				halo_exchange( L, z, static_cast< int >( k ) );
 				return;
@@ -361,7 +363,7 @@ namespace slabgpu {
 			int64_t nb = 0;
 			const int32_t * bpos = halo_boundary_positions( L->plan, static_cast< int >( k ), &nb );
 			if( nb > 0 ) {
-				kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				kern::gs_color_step( ctx->stream, L->colorA, L->d_rows,
 					L->color_pos[ k ], nb, z->d, r->d, flags, src, out, zero, 0, bpos, nullptr );
 			}
 			const bool comm = halo_has_comm( ctx );
@@ -369,7 +371,7 @@ namespace slabgpu {
 				halo_fork( ctx );
 				halo_exchange_plan( ctx, L->plan, z, static_cast< int >( k ), halo_comm_stream( ctx ) );
 			}
-			kern::gs_color_step( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+			kern::gs_color_step( ctx->stream, L->colorA, L->d_rows,
 				L->color_pos[ k ], count, z->d, r->d, flags, src, out, zero, window, nullptr, halo_boundary_flags( L->plan ) );
 			if( comm ) {
 				halo_join( ctx );
@@ -642,7 +644,7 @@ namespace slabgpu {
 			if( L->coarser ) {
 				if( ctx->fused_transfers && L->is_stencil ) {
 					Span transfer( ctx, &L->stats.transfer_ns ); // residual + restriction in one kernel
-					kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+					kern::residual_restrict( ctx->stream, L->colorA, L->d_rows,
 						static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d, nullptr );
 				} else {
 					op_mxv( L->f.get(), nullptr, L->A.get(), z, SLAB_DESC_NONE );
@@ -711,7 +713,7 @@ namespace slabgpu {
 			// launch keeps its matrix rows in registers, else they are one extra pass over the colour-0
 			// rows; the prolongation rides on the FIRST colour step of the post-smoother (forward, colour
 			// 0), which reads no other colour-0 value. Results are bit-identical to the composition above.
-			const bool fuse_residual = kern::gs_color_step_can_fuse_residual( static_cast< int64_t >( L->color_size[ 0 ] ) );
+			const bool fuse_residual = kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ 0 ] ) );
 			const bool ghosts = L->z_c->n_alloc > L->z_c->n; // distributed: the ghost tail must be zeroed too
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
 				forward_enqueue( L, z, r );
@@ -721,7 +723,7 @@ namespace slabgpu {
 				}
 			}
 			if( !fuse_residual ) {
-				kern::residual_restrict( ctx->stream, L->colorA.slice_off, L->colorA.vals, L->colorA.cols, L->d_rows,
+				kern::residual_restrict( ctx->stream, L->colorA, L->d_rows,
 					static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d, L->z_c->d );
 			}
 			if( ghosts ) {

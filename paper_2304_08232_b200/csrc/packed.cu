@@ -1,0 +1,655 @@
+// packed.cu — dictionary-coded SELL: the matrix stream of the hot kernels cut from 12 bytes to 1 byte
+// per stored entry, with results that are bit-identical to the plain format.
+//
+// Why. Every product and colour step of the solve is bound by the matrix stream (12 B per entry against
+// 8 B per row of vector traffic). A matrix handed to the library is immutable and opaque
+// (sparse_matrix.hpp:48-171), so its device copy may be any lossless encoding. Matrices that come from
+// a discretisation repeat very few distinct (column - row, value) pairs — the 27-point operator of this
+// benchmark has 27 — so each entry is stored as the 8-bit index of its pair in a per-matrix dictionary
+// that is discovered from the entries themselves (no knowledge of where the matrix came from). The
+// decode is exact: the value is the dictionary's double, the column is row + delta in integers, and the
+// entries of a row are visited in the same ascending-column order (operations.hpp:116-125). Rows with
+// an entry outside the dictionary (ghost columns of a decomposed level, irregular matrices) are
+// flagged and read from the plain arrays by the same thread. Matrices that do not compress keep the
+// plain kernels.
+//
+// With the stream 12x smaller, a fine-level colour step stops evicting the vector it gathers from the
+// L2; what bounds the kernels then is instruction issue and the L1/L2 gather path, so the decode is kept
+// to a handful of instructions per entry: one 16-byte shared-memory read yields value and offset, full
+// rows (no padding inside the width class) skip the per-entry padding test, and the diagonal a colour
+// step divides by is named by a spare byte of the row instead of being searched for.
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "device_util.cuh"
+
+namespace slabgpu {
+
+	int g_use_packed = 1;
+	int g_pack_build = 1;
+	int g_packed_block = 256;
+	int g_packed_batch = 1;              // words (of 4 codes) gathered together by many-wave launches
+	int64_t g_packed_deep_rows = 0;      // launches below this many rows gather the whole row at once (measured:
+	                                     // never better than the short batches once the dictionary left shared memory)
+	int64_t g_packed_min_rows = 65536;   // launches below this many rows use the plain kernels (measured: their
+	                                     // matrices sit in the L2, where the plain preload shape is faster)
+
+	void Packed::release() {
+		if( codes ) cudaFree( codes );
+		if( dict ) cudaFree( dict );
+		delete[] h_dict;
+		codes = nullptr;
+		dict = nullptr;
+		h_dict = nullptr;
+		max_width = ncodes = chunks = dict_size = 0;
+		escaped_rows = 0;
+	}
+
+	namespace kern {
+
+		namespace {
+
+			using namespace dev;
+
+			constexpr int kDict = 256;
+			constexpr unsigned int kEscape = 255u;
+			constexpr int kMaxCodes = 64;
+			constexpr int kMaxChunks = ( kMaxCodes + 16 ) / 16;
+
+			// width classes the kernels are instantiated for
+			int width_class( int max_width ) {
+				const int classes[] = { 8, 16, 27, 32, 64 };
+				for( int c : classes ) {
+					if( max_width <= c ) {
+						return c;
+					}
+				}
+				return 0;
+			}
+
+			// ------------------------------------------------------------ encoder (setup)
+
+			// one thread per row position: looks every entry up in the dictionary and writes the row's
+			// codes; entries that are missing flag the row and are offered as candidates
+			__global__ void __launch_bounds__( kBlock ) k_pack_rows( const int64_t * __restrict__ slice_off,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
+				int64_t npos, int64_t npadded, const DictEntry * __restrict__ dict, int dict_size, int chunks,
+				uint4 * __restrict__ codes, unsigned long long * escaped, unsigned long long * cand_key, unsigned int cand_cap,
+				double * cand_val, int32_t * cand_delta ) {
+				__shared__ long long s_val[ kDict ];
+				__shared__ int32_t s_delta[ kDict ];
+				for( int t = threadIdx.x; t < dict_size; t += blockDim.x ) {
+					s_val[ t ] = __double_as_longlong( dict[ t ].val );
+					s_delta[ t ] = dict[ t ].delta;
+				}
+				__syncthreads();
+				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( pos >= npadded ) {
+					return;
+				}
+				const int64_t s = pos >> 5;
+				const int lane = static_cast< int >( pos & 31 );
+				const int64_t row = pos < npos ? ( rows != nullptr ? static_cast< int64_t >( rows[ pos ] ) : pos ) : -1;
+				unsigned int w[ 4 * kMaxChunks ];
+				#pragma unroll
+				for( int j = 0; j < 4 * kMaxChunks; ++j ) {
+					w[ j ] = 0u;
+				}
+				bool escape = false;
+				unsigned int diag_code = 0u;
+				if( row >= 0 ) {
+					const int64_t base = slice_off[ s ];
+					const int width = static_cast< int >( ( slice_off[ s + 1 ] - base ) >> 5 );
+					for( int k = 0; k < width; ++k ) {
+						const int64_t e = base + static_cast< int64_t >( k ) * kSlice + lane;
+						const int32_t c = cols[ e ];
+						if( c < 0 ) {
+							continue; // padding keeps code 0
+						}
+						const long long bits = __double_as_longlong( vals[ e ] );
+						const int32_t delta = c - static_cast< int32_t >( row );
+						unsigned int code = 0u;
+						for( int t = 1; t < dict_size; ++t ) {
+							if( s_delta[ t ] == delta && s_val[ t ] == bits ) {
+								code = static_cast< unsigned int >( t );
+								break;
+							}
+						}
+						if( delta == 0 ) {
+							diag_code = code;
+						}
+						if( code == 0u ) {
+							escape = true;
+							// offer the pair: open-addressing set keyed by a 64-bit mix of the pair. (Two different
+							// pairs with one key are vanishingly rare and only delay the second by a round.)
+							unsigned long long key = ( static_cast< unsigned long long >( bits ) * 0x9E3779B97F4A7C15ull )
+								^ ( static_cast< unsigned long long >( static_cast< uint32_t >( delta ) ) * 0xC2B2AE3D27D4EB4Full );
+							key |= 1ull;
+							unsigned int slot = static_cast< unsigned int >( ( key >> 20 ) % cand_cap );
+							for( unsigned int probe = 0; probe < 64u; ++probe ) {
+								const unsigned long long cur = reinterpret_cast< volatile unsigned long long * >( cand_key )[ slot ];
+								if( cur == key ) {
+									break;
+								}
+								if( cur == 0ull ) {
+									const unsigned long long old = atomicCAS( cand_key + slot, 0ull, key );
+									if( old == 0ull ) {
+										cand_val[ slot ] = vals[ e ];
+										cand_delta[ slot ] = delta;
+										break;
+									}
+									if( old == key ) {
+										break;
+									}
+								}
+								slot = slot + 1 == cand_cap ? 0u : slot + 1;
+							}
+						}
+						#pragma unroll
+						for( int j = 0; j < 4 * kMaxChunks; ++j ) { // static indexing keeps w in registers
+							if( j == ( k >> 2 ) ) {
+								w[ j ] |= code << ( 8 * ( k & 3 ) );
+							}
+						}
+					}
+				}
+				if( escape ) {
+					w[ 0 ] = ( w[ 0 ] & ~0xffu ) | kEscape;
+					atomicAdd( escaped, 1ull );
+				}
+				#pragma unroll
+				for( int j = 0; j < 4 * kMaxChunks; ++j ) { // the row's last byte names its diagonal entry
+					if( j == 4 * chunks - 1 ) {
+						w[ j ] |= diag_code << 24;
+					}
+				}
+				#pragma unroll
+				for( int j = 0; j < kMaxChunks; ++j ) {
+					if( j < chunks ) {
+						codes[ ( s * chunks + j ) * kSlice + lane ] = make_uint4( w[ 4 * j ], w[ 4 * j + 1 ], w[ 4 * j + 2 ], w[ 4 * j + 3 ] );
+					}
+				}
+			}
+
+			// ------------------------------------------------------------ decoder
+
+			template< int CHUNKS >
+			struct RowCodes {
+				uint4 q[ CHUNKS ];
+				__device__ __forceinline__ unsigned int word( int wi ) const {
+					const uint4 & v = q[ wi >> 2 ];
+					switch( wi & 3 ) {
+						case 0: return v.x;
+						case 1: return v.y;
+						case 2: return v.z;
+						default: return v.w;
+					}
+				}
+				__device__ __forceinline__ bool escaped() const {
+					return ( q[ 0 ].x & 0xffu ) == kEscape;
+				}
+				__device__ __forceinline__ unsigned int diag_code() const {
+					return q[ CHUNKS - 1 ].w >> 24;
+				}
+				// does any of the first NCODES codes say "padding"? (rows narrower than the width class)
+				template< int NCODES >
+				__device__ __forceinline__ bool ragged() const {
+					constexpr int WORDS = ( NCODES + 3 ) / 4;
+					unsigned int hit = 0u;
+					#pragma unroll
+					for( int wi = 0; wi < WORDS; ++wi ) {
+						unsigned int w = word( wi );
+						if( wi == WORDS - 1 && ( NCODES & 3 ) != 0 ) {
+							w |= 0xffffffffu << ( 8 * ( NCODES & 3 ) );
+						}
+						hit |= ( w - 0x01010101u ) & ~w & 0x80808080u; // non-zero iff some byte of w is zero
+					}
+					return hit != 0u;
+				}
+			};
+
+			template< int CHUNKS >
+			__device__ __forceinline__ void codes_load( const uint4 * __restrict__ codes, int64_t pos, RowCodes< CHUNKS > & rc ) {
+				const uint4 * p = codes + ( ( pos >> 5 ) * CHUNKS ) * kSlice + ( pos & 31 );
+				#pragma unroll
+				for( int j = 0; j < CHUNKS; ++j ) {
+					rc.q[ j ] = __ldcs( p + j * kSlice );
+				}
+			}
+
+			// The dictionary travels as a kernel parameter and is read with indexed constant loads: the 32
+			// rows of an interior slice carry the same codes, so the index is warp-uniform and the read costs
+			// one constant-cache access — unlike a shared-memory table, it takes nothing from the L1 data
+			// pipe, which the gathers saturate (measured: shared-memory lookups were 45% of its wavefronts).
+			template< int DICT >
+			struct DictParam {
+				double val[ DICT ];
+				int32_t delta[ DICT ];
+			};
+
+			// ordered row sum over the coded entries: acc = acc + val*xrow[delta] (xrow = x + row), ascending
+			// column order. RAGGED rows test every code for padding (code 0 is skipped); full rows do not.
+			// The gathers of BATCH 4-code words go out before their add chain runs: a large BATCH suits
+			// latency-bound small launches (every gather of the row in flight at once), a small one keeps
+			// the register count low for many-wave launches.
+			template< int NCODES, int CHUNKS, int BATCH, bool RAGGED, int DICT >
+			__device__ __forceinline__ double coded_row_sum( const RowCodes< CHUNKS > & rc, const double * xrow,
+				const DictParam< DICT > & dp ) {
+				constexpr int WORDS = ( NCODES + 3 ) / 4;
+				double acc = 0.0;
+				#pragma unroll
+				for( int w0 = 0; w0 < WORDS; w0 += BATCH ) {
+					double xv[ 4 * BATCH ];
+					#pragma unroll
+					for( int b = 0; b < BATCH; ++b ) {
+						#pragma unroll
+						for( int j = 0; j < 4; ++j ) {
+							if( 4 * ( w0 + b ) + j < NCODES ) {
+								const unsigned int code = ( rc.word( w0 + b ) >> ( 8 * j ) ) & 0xffu;
+								xv[ 4 * b + j ] = xrow[ dp.delta[ code ] ];
+							}
+						}
+					}
+					// keep the batch's gathers together, ahead of the add chain: the assembler schedules within
+					// basic blocks, so a never-taken branch pins them (an empty asm only pins the front end)
+					if( BATCH > 1 ) {
+						asm volatile( "" ::: "memory" );
+						if( dp.delta[ 0 ] == 0x7fffffff ) { // entry 0 is {0.0, 0}
+							__trap();
+						}
+					}
+					#pragma unroll
+					for( int b = 0; b < BATCH; ++b ) {
+						#pragma unroll
+						for( int j = 0; j < 4; ++j ) {
+							if( 4 * ( w0 + b ) + j < NCODES ) {
+								const unsigned int code = ( rc.word( w0 + b ) >> ( 8 * j ) ) & 0xffu;
+								const double sum = __dadd_rn( acc, __dmul_rn( dp.val[ code ], xv[ 4 * b + j ] ) );
+								if( RAGGED ) {
+									acc = code != 0u ? sum : acc;
+								} else {
+									acc = sum;
+								}
+							}
+						}
+					}
+				}
+				return acc;
+			}
+
+			// the same sum for an escaped row, from the plain SELL arrays
+			template< bool WANT_DIAG >
+			__device__ __noinline__ double plain_row_sum( const int64_t * __restrict__ slice_off, const double * __restrict__ vals,
+				const int32_t * __restrict__ cols, int64_t pos, const double * x, int32_t diag_row, double & diag ) {
+				const int64_t s = pos >> 5;
+				const int64_t begin = slice_off[ s ] + ( pos & 31 );
+				const int64_t end = slice_off[ s + 1 ];
+				double acc = 0.0;
+				for( int64_t e = begin; e < end; e += kSlice ) {
+					const int32_t c = cols[ e ];
+					const double v = vals[ e ];
+					if( c >= 0 ) {
+						acc = __dadd_rn( acc, __dmul_rn( v, x[ c ] ) );
+						if( WANT_DIAG && c == diag_row ) {
+							diag = v;
+						}
+					}
+				}
+				return acc;
+			}
+
+			struct PlainRef { // the plain arrays, for escaped rows
+				const int64_t * slice_off;
+				const double * vals;
+				const int32_t * cols;
+			};
+
+			// row sum of any packed row: escaped -> plain arrays (rare, divergent); otherwise the warp takes
+			// ONE path — the padding-testing one if any of its rows is narrower than the width class, the
+			// test-free one if none is (`warp_ragged` is a warp vote taken by the caller)
+			template< int NCODES, int CHUNKS, int BATCH, bool WANT_DIAG, int DICT >
+			__device__ __forceinline__ double any_row_sum( const RowCodes< CHUNKS > & rc, bool warp_ragged, const PlainRef & plain,
+				int64_t pos, int32_t row, const double * x, const DictParam< DICT > & dp, double & diag ) {
+				if( rc.escaped() ) {
+					return plain_row_sum< WANT_DIAG >( plain.slice_off, plain.vals, plain.cols, pos, x, row, diag );
+				}
+				if( WANT_DIAG ) {
+					diag = dp.val[ rc.diag_code() ];
+				}
+				if( warp_ragged ) {
+					return coded_row_sum< NCODES, CHUNKS, BATCH, true >( rc, x + row, dp );
+				}
+				return coded_row_sum< NCODES, CHUNKS, BATCH, false >( rc, x + row, dp );
+			}
+
+			// ------------------------------------------------------------ kernels
+
+			// operations.hpp:164-174; MASKED: one thread per mask member, others untouched.
+			// (x and y deliberately without __restrict__: ordinary loads obey the scheduling fence in coded_row_sum)
+			template< int NCODES, int CHUNKS, int BATCH, bool MASKED, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_spmv_packed( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const double * x, double * y,
+				const int32_t * __restrict__ members, int64_t count, double * dot_partials ) {
+				__shared__ double smem[ 32 ];
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const bool live = k < count;
+				int64_t row = 0;
+				RowCodes< CHUNKS > rc;
+				if( live ) {
+					row = MASKED ? members[ k ] : k;
+					codes_load( codes, row, rc );
+				}
+				dep_trigger();
+				dep_wait();
+				double prod = 0.0;
+				if( live ) {
+					const bool warp_ragged = __any_sync( __activemask(), rc.template ragged< NCODES >() );
+					double unused = 0.0;
+					const double acc = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, row, static_cast< int32_t >( row ), x, dp, unused );
+					y[ row ] = acc;
+					prod = dot_partials != nullptr ? __dmul_rn( x[ row ], acc ) : 0.0;
+				}
+				if( dot_partials != nullptr ) { // x'(A x): block partials, folded by sum_partials (cg.hpp:122-123)
+					const double block_sum = block_tree_sum( prod, smem );
+					if( threadIdx.x == 0 ) {
+						dot_partials[ blockIdx.x ] = block_sum;
+					}
+				}
+			}
+
+			// smoother.hpp:60-72 fused, with the grid transfers of kernels.cu's k_gs_color riding on the
+			// colour-0 steps (flags bit 0: prolongation in front, bit 1: residual + restriction behind)
+			template< int NCODES, int CHUNKS, int BATCH, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
+				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				int32_t i = -1;
+				int64_t pos = 0;
+				RowCodes< CHUNKS > rc;
+				if( k < pos_count ) {
+					pos = pos_list != nullptr ? pos_list[ k ] : pos_begin + k;
+					// rows == nullptr: vectors in position order (row index == position)
+					i = skip != nullptr && skip[ pos ] ? -1 : ( rows != nullptr ? rows[ pos ] : static_cast< int32_t >( pos ) );
+					codes_load( codes, pos, rc );
+				}
+				dep_trigger();
+				dep_wait();
+				if( i < 0 ) {
+					return;
+				}
+				const bool warp_ragged = __any_sync( __activemask(), rc.template ragged< NCODES >() );
+				const int64_t coarse = pos - pos_begin;
+				const double ri = r[ i ];
+				double zi = z[ i ];
+				if( flags & 1 ) {
+					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ coarse ] ) );
+					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+					z[ i ] = zi;
+				}
+				double d = 0.0;
+				const double s = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, z, dp, d );
+				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+				if( flags & 2 ) {
+					double unused = 0.0;
+					const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, z, dp, unused );
+					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
+					out[ coarse ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+					zero[ coarse ] = 0.0;
+				}
+			}
+
+			// multigrid.hpp:100-104 on the injected rows (the colour-0 block): r_c[p] = 0 + 1*(1*r[i] + (-1)*(A z)[i])
+			template< int NCODES, int CHUNKS, int BATCH, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_packed( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
+				int64_t n_coarse, const double * z, const double * __restrict__ r, double * r_c, double * zero ) {
+				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const bool live = p < n_coarse;
+				int32_t i = 0;
+				RowCodes< CHUNKS > rc;
+				if( live ) {
+					i = rows[ p ];
+					codes_load( codes, p, rc );
+				}
+				dep_trigger();
+				dep_wait();
+				if( !live ) {
+					return;
+				}
+				const bool warp_ragged = __any_sync( __activemask(), rc.template ragged< NCODES >() );
+				double unused = 0.0;
+				const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, p, i, z, dp, unused );
+				const double f = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -1.0, az ) );
+				r_c[ p ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+				if( zero != nullptr ) {
+					zero[ p ] = 0.0; // set_all(z_c, 0), multigrid.hpp:104
+				}
+			}
+
+			// ------------------------------------------------------------ dispatch on the width class
+
+			// batch: words whose gathers are in flight together (`deep`: the whole row); dictionary capacity
+			// of the parameter block: 32 entries (384 bytes) when that is enough, else all 256 (3 KB)
+			template< int N, int D, class F >
+			void by_batch( bool deep, F && f ) {
+				constexpr int C = ( N + 16 ) / 16;
+				constexpr int W = ( N + 3 ) / 4;
+				if( deep ) {
+					f( std::integral_constant< int, N >(), std::integral_constant< int, C >(), std::integral_constant< int, W >(),
+						std::integral_constant< int, D >() );
+				} else if( g_packed_batch >= 2 && W > 2 ) {
+					f( std::integral_constant< int, N >(), std::integral_constant< int, C >(), std::integral_constant< int, 2 >(),
+						std::integral_constant< int, D >() );
+				} else {
+					f( std::integral_constant< int, N >(), std::integral_constant< int, C >(), std::integral_constant< int, 1 >(),
+						std::integral_constant< int, D >() );
+				}
+			}
+			template< int D, class F >
+			void by_width( int ncodes, bool deep, F && f ) {
+				switch( ncodes ) {
+					case 8: by_batch< 8, D >( deep, f ); break;
+					case 16: by_batch< 16, D >( deep, f ); break;
+					case 27: by_batch< 27, D >( deep, f ); break;
+					case 32: by_batch< 32, D >( deep, f ); break;
+					case 64: by_batch< 64, D >( deep, f ); break;
+					default: fail( SLAB_ERR_INTERNAL, "packed matrix with an unknown width class" );
+				}
+			}
+			template< class F >
+			void by_shape( const Packed & P, bool deep, F && f ) {
+				if( P.dict_size <= 32 ) {
+					by_width< 32 >( P.ncodes, deep, f );
+				} else {
+					by_width< 256 >( P.ncodes, deep, f );
+				}
+			}
+			template< int DICT >
+			DictParam< DICT > dict_param( const Packed & P ) {
+				DictParam< DICT > dp;
+				for( int t = 0; t < DICT; ++t ) {
+					dp.val[ t ] = t < P.dict_size ? P.h_dict[ t ].val : 0.0;
+					dp.delta[ t ] = t < P.dict_size ? P.h_dict[ t ].delta : 0;
+				}
+				return dp;
+			}
+
+			int block_size() {
+				return g_packed_block == 128 ? 128 : 256;
+			}
+			// launches of fewer rows than this are latency-bound: every gather of a row goes out at once
+			bool deep_for( int64_t rows ) {
+				return rows < g_packed_deep_rows;
+			}
+
+		} // namespace
+
+		void spmv_packed( cudaStream_t st, const Sell & S, const double * x, double * y, const int32_t * members,
+			int64_t count, double * dot_partials, double * dot_out ) {
+			const Packed & P = S.packed;
+			const PlainRef plain{ S.slice_off, S.vals, S.cols };
+			const int block = block_size();
+			const unsigned int grid = blocks_for( count, block );
+			by_shape( P, deep_for( count ), [ & ]( auto N, auto C, auto B, auto D ) {
+				const auto dp = dict_param< D.value >( P );
+				if( members != nullptr ) {
+					launch_pdl( k_spmv_packed< N.value, C.value, B.value, true, D.value >, grid, block, st, P.codes, dp, plain,
+						x, y, members, count, static_cast< double * >( nullptr ) );
+				} else {
+					launch_pdl( k_spmv_packed< N.value, C.value, B.value, false, D.value >, grid, block, st, P.codes, dp, plain,
+						x, y, members, count, dot_out != nullptr ? dot_partials : nullptr );
+				}
+			} );
+			if( members == nullptr && dot_out != nullptr ) {
+				sum_partials( st, dot_partials, grid, dot_out );
+			}
+		}
+
+		void gs_color_step_packed( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t pos_begin, int64_t pos_count,
+			double * z, const double * r, int flags, const double * src, double * out, double * zero, const int32_t * pos_list,
+			const uint8_t * skip ) {
+			const Packed & P = S.packed;
+			const PlainRef plain{ S.slice_off, S.vals, S.cols };
+			const int block = block_size();
+			by_shape( P, deep_for( pos_count ), [ & ]( auto N, auto C, auto B, auto D ) {
+				launch_pdl( k_gs_color_packed< N.value, C.value, B.value, D.value >, blocks_for( pos_count, block ), block, st, P.codes,
+					dict_param< D.value >( P ), plain, rows, pos_begin, pos_count, z, r, flags, src, out, zero, pos_list, skip );
+			} );
+		}
+
+		void residual_restrict_packed( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t n_coarse, const double * z,
+			const double * r, double * r_c, double * zero ) {
+			const Packed & P = S.packed;
+			const PlainRef plain{ S.slice_off, S.vals, S.cols };
+			const int block = block_size();
+			by_shape( P, deep_for( n_coarse ), [ & ]( auto N, auto C, auto B, auto D ) {
+				launch_pdl( k_residual_restrict_packed< N.value, C.value, B.value, D.value >, blocks_for( n_coarse, block ), block, st,
+					P.codes, dict_param< D.value >( P ), plain, rows, n_coarse, z, r, r_c, zero );
+			} );
+		}
+
+	} // namespace kern
+
+	// ---------------------------------------------------------------- building the packed copy
+
+	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows ) {
+		using namespace kern;
+		S.packed.release();
+		const int ncodes = width_class( S.max_width );
+		if( !g_pack_build || S.nrows == 0 || S.entries == 0 || S.max_width < 1 || ncodes == 0 ) {
+			return;
+		}
+		Packed P;
+		P.max_width = S.max_width;
+		P.ncodes = ncodes;
+		P.chunks = ( ncodes + 16 ) / 16;
+		const int64_t npadded = S.nslices * kSlice;
+		constexpr unsigned int kCandCap = 2048;
+		unsigned long long * d_escaped = nullptr;
+		unsigned long long * d_cand_key = nullptr;
+		double * d_cand_val = nullptr;
+		int32_t * d_cand_delta = nullptr;
+		cudaStream_t st = ctx->stream;
+		try {
+			SLAB_CUDA( cudaMalloc( &P.codes, static_cast< size_t >( npadded ) * P.chunks * sizeof( uint4 ) ) );
+			SLAB_CUDA( cudaMalloc( &P.dict, kDict * sizeof( DictEntry ) ) );
+			SLAB_CUDA( cudaMalloc( &d_escaped, sizeof( unsigned long long ) ) );
+			SLAB_CUDA( cudaMalloc( &d_cand_key, kCandCap * sizeof( unsigned long long ) ) );
+			SLAB_CUDA( cudaMalloc( &d_cand_val, kCandCap * sizeof( double ) ) );
+			SLAB_CUDA( cudaMalloc( &d_cand_delta, kCandCap * sizeof( int32_t ) ) );
+			std::vector< DictEntry > dict( kDict, DictEntry{ 0.0, 0, 0 } );
+			std::set< std::pair< int32_t, uint64_t > > known;
+			int dict_size = 1; // entry 0: padding
+			unsigned long long escaped = 0;
+			for( int round = 0;; ++round ) {
+				upload_sync( st, P.dict, dict.data(), kDict * sizeof( DictEntry ) );
+				SLAB_CUDA( cudaMemsetAsync( d_escaped, 0, sizeof( unsigned long long ), st ) );
+				SLAB_CUDA( cudaMemsetAsync( d_cand_key, 0, kCandCap * sizeof( unsigned long long ), st ) );
+				k_pack_rows<<< dev::blocks_for( npadded ), dev::kBlock, 0, st >>>( S.slice_off, S.vals, S.cols, d_rows, S.nrows, npadded,
+					P.dict, dict_size, P.chunks, P.codes, d_escaped, d_cand_key, kCandCap, d_cand_val, d_cand_delta );
+				SLAB_CUDA( cudaGetLastError() );
+				count_launch();
+				SLAB_CUDA( cudaMemcpyAsync( &escaped, d_escaped, sizeof( escaped ), cudaMemcpyDeviceToHost, st ) );
+				SLAB_CUDA( cudaStreamSynchronize( st ) );
+				if( escaped == 0 || round == 7 || dict_size == kDict - 1 ) {
+					break;
+				}
+				std::vector< unsigned long long > ck( kCandCap );
+				std::vector< double > cv( kCandCap );
+				std::vector< int32_t > cd( kCandCap );
+				SLAB_CUDA( cudaMemcpyAsync( ck.data(), d_cand_key, kCandCap * sizeof( unsigned long long ), cudaMemcpyDeviceToHost, st ) );
+				SLAB_CUDA( cudaMemcpyAsync( cv.data(), d_cand_val, kCandCap * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+				SLAB_CUDA( cudaMemcpyAsync( cd.data(), d_cand_delta, kCandCap * sizeof( int32_t ), cudaMemcpyDeviceToHost, st ) );
+				SLAB_CUDA( cudaStreamSynchronize( st ) );
+				// new pairs in a reproducible order (the set is filled in arrival order): narrow bands first,
+				// so that when the dictionary cannot hold everything the far-away columns (ghost slots of a
+				// decomposed level) are the ones left to the plain path
+				const auto band_order = []( const std::pair< int32_t, uint64_t > & a, const std::pair< int32_t, uint64_t > & b ) {
+					const int64_t da = a.first < 0 ? -static_cast< int64_t >( a.first ) : a.first;
+					const int64_t db = b.first < 0 ? -static_cast< int64_t >( b.first ) : b.first;
+					return da != db ? da < db : a < b;
+				};
+				std::set< std::pair< int32_t, uint64_t >, decltype( band_order ) > fresh( band_order );
+				for( unsigned int t = 0; t < kCandCap; ++t ) {
+					if( ck[ t ] == 0ull ) {
+						continue;
+					}
+					uint64_t bits;
+					std::memcpy( &bits, &cv[ t ], sizeof( bits ) );
+					const std::pair< int32_t, uint64_t > key( cd[ t ], bits );
+					if( !known.count( key ) ) {
+						fresh.insert( key );
+					}
+				}
+				bool grew = false;
+				for( const auto & key : fresh ) {
+					if( dict_size >= kDict - 1 ) {
+						break;
+					}
+					known.insert( key );
+					dict[ dict_size ].delta = key.first;
+					std::memcpy( &dict[ dict_size ].val, &key.second, sizeof( double ) );
+					++dict_size;
+					grew = true;
+				}
+				if( !grew ) {
+					break;
+				}
+			}
+			P.dict_size = dict_size;
+			P.escaped_rows = static_cast< int64_t >( escaped );
+			P.h_dict = new DictEntry[ kDict ];
+			std::copy( dict.begin(), dict.end(), P.h_dict );
+		} catch( ... ) {
+			cudaFree( d_escaped );
+			cudaFree( d_cand_key );
+			cudaFree( d_cand_val );
+			cudaFree( d_cand_delta );
+			P.release();
+			throw;
+		}
+		cudaFree( d_escaped );
+		cudaFree( d_cand_key );
+		cudaFree( d_cand_val );
+		cudaFree( d_cand_delta );
+		// not worth it when many rows would take the plain path anyway (each costs both code paths)
+		if( P.escaped_rows * 8 > S.nrows ) {
+			P.release();
+			return;
+		}
+		S.packed = P;
+	}
+
+} // namespace slabgpu

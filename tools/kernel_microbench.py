@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--sets", nargs="*", default=None,
+                    help="tuning sets to time, each 'key=value,key=value' (slab_set_tuning keys), e.g. packed=0 packed=1,packed_block=512")
     args = ap.parse_args()
     dims = tuple(args.dims)
     peak = 6551.0
@@ -66,8 +68,11 @@ def main():
             out["checksums_match_reference_bitwise"] = ok
             print("checksums match the reference bitwise:", ok, sums)
 
-    for variant in args.variants:
-        _capi.set_tuning("stream_variant", variant)
+    runs = [("stream_variant=%d" % v) for v in args.variants] if args.sets is None else args.sets
+    for variant in runs:
+        for pair in variant.split(","):
+            key, value = pair.split("=")
+            _capi.set_tuning(key, int(value))
         for _ in range(3):
             slab.mxv(y, lvl.A, x)
         ctx.timer_start()
