@@ -71,7 +71,11 @@ int slab_set_programmatic_launch( int enabled );
 /* performance knobs that never change results: "stream_rows" (launches with at least this many rows
  * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl", "halo_overlap" (boundary
  * rows first, halo messages beside the interior rows), "persist_rows" / "persist_blocks_per_sm" (persistent
- * coarse-level kernel), "l2_window". Process-wide; each also has an environment variable SLAB_<KEY>. */
+ * coarse-level kernel), "l2_window"; for the dictionary-coded matrix copy: "packed" (use it, default 1),
+ * "pack_build" (build it when a matrix is created, default 1), "packed_min_rows" (smaller launches use the
+ * plain arrays), "packed_batch", "packed_block", "packed_rows" / "packed_rows_spmv" (rows per thread of
+ * colour steps / products), "packed_multi_min_rows". Process-wide; each also has an environment variable
+ * SLAB_<KEY> for the first four packed keys and the older ones. */
 int slab_set_tuning( const char * key, int64_t value );
 
 /* ------------------------------------------------------------------ context */
@@ -122,6 +126,19 @@ int slab_mat_shape( slab_mat_t A, uint64_t * nrows, uint64_t * ncols, uint64_t *
 int slab_mat_download_csr( slab_mat_t A, uint64_t * row_offsets, uint64_t * col_indices, double * values );
 /* bytes the opaque format occupies in HBM (values + indices + slice table) */
 int slab_mat_device_bytes( slab_mat_t A, uint64_t * bytes );
+/* How the matrix is held on the device. Every matrix has the plain SELL-32 arrays (12 bytes per stored
+ * entry); matrices with few distinct (column - row, value) pairs also get a dictionary-coded copy (1 byte
+ * per entry) that the kernels read instead — same arithmetic, same order, same bits. */
+typedef struct slab_format_info {
+	int32_t packed;         /* 1 when the dictionary-coded copy exists */
+	int32_t width_class;    /* codes per row the kernels are instantiated for (>= widest row), 0 if not packed */
+	int32_t dict_size;      /* dictionary entries in use (entry 0 = padding) */
+	int32_t stride;         /* slices between rows that mostly repeat their codes (multi-row kernels), 0 = none */
+	int64_t escaped_rows;   /* rows with an entry outside the dictionary: read from the plain arrays */
+	uint64_t plain_bytes;   /* bytes of the plain arrays */
+	uint64_t packed_bytes;  /* bytes of the coded copy */
+} slab_format_info;
+int slab_mat_format_info( slab_mat_t A, slab_format_info * out );
 
 /* ------------------------------------------------------------------ masks (index_mask.hpp) */
 int slab_mask_create( slab_ctx_t ctx, uint64_t universe, const uint64_t * members, uint64_t count,
@@ -159,6 +176,8 @@ typedef struct slab_level_stats { /* LevelStats problem.hpp:204-209; times from 
 	uint64_t nnz_visited;
 } slab_level_stats;
 int slab_level_stats_get( slab_level_t level, slab_level_stats * out );
+/* format of the level's colour-major matrix copy (the one the smoother reads) */
+int slab_level_format_info( slab_level_t level, slab_format_info * out );
 int slab_level_stats_reset( slab_level_t level ); /* reset_stats problem.hpp:271-276 */
 
 /* ------------------------------------------------------------------ smoother (smoother.hpp) */

@@ -80,6 +80,14 @@ class _CgResult(C.Structure):
     _fields_ = [("iterations", C.c_uint64), ("converged", C.c_int), ("solve_ms", C.c_double)]
 
 
+class FormatInfo(C.Structure):  # slab_format_info
+    _fields_ = [("packed", C.c_int32), ("width_class", C.c_int32), ("dict_size", C.c_int32), ("stride", C.c_int32),
+                ("escaped_rows", C.c_int64), ("plain_bytes", C.c_uint64), ("packed_bytes", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class _LevelStats(C.Structure):
     _fields_ = [("smoother_ns", C.c_uint64), ("transfer_ns", C.c_uint64), ("mg_ns", C.c_uint64),
                 ("nnz_visited", C.c_uint64)]
@@ -127,6 +135,8 @@ SIGNATURES = {
     "slab_mat_shape": (C.c_int, [_vp, _pu64, _pu64, _pu64]),
     "slab_mat_download_csr": (C.c_int, [_vp, _vp, _vp, _vp]),
     "slab_mat_device_bytes": (C.c_int, [_vp, _pu64]),
+    "slab_mat_format_info": (C.c_int, [_vp, _vp]),
+    "slab_level_format_info": (C.c_int, [_vp, _vp]),
     "slab_mask_create": (C.c_int, [_vp, _u64, _vp, _u64, _pvp]),
     "slab_mask_destroy": (C.c_int, [_vp]),
     "slab_mask_info": (C.c_int, [_vp, _pu64, _pu64]),
@@ -487,6 +497,11 @@ class SparseMatrix:  # sparse_matrix.hpp:48-171
         _check(_lib.slab_mat_device_bytes(self._h, C.byref(b)))
         return b.value
 
+    def format_info(self) -> dict:
+        info = FormatInfo()
+        _check(_lib.slab_mat_format_info(self._h, C.byref(info)))
+        return info.as_dict()
+
 
 class IndexMask:  # index_mask.hpp:35-73
     def __init__(self, ctx: Context, universe_size: int, members: Sequence[int]):
@@ -624,6 +639,12 @@ class ProblemLevel:  # problem.hpp:220-277
 
     def reset_stats(self) -> None:
         _check(_lib.slab_level_stats_reset(self._h))
+
+    def format_info(self) -> dict:
+        """format of the colour-major matrix copy the smoother reads"""
+        info = FormatInfo()
+        _check(_lib.slab_level_format_info(self._h, C.byref(info)))
+        return info.as_dict()
 
     # ---- domain decomposition: manual halo access (tests, custom transports)
     def decomp(self) -> dict:

@@ -93,10 +93,14 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_pack_build = value ? 1 : 0;
 		} else if( k == "packed_block" ) {
 			g_packed_block = static_cast< int >( value );
+		} else if( k == "packed_rows" ) {
+			g_packed_rows = static_cast< int >( value );
+		} else if( k == "packed_rows_spmv" ) {
+			g_packed_rows_spmv = static_cast< int >( value );
+		} else if( k == "packed_multi_min_rows" ) {
+			g_packed_multi_min_rows = value;
 		} else if( k == "packed_batch" ) {
 			g_packed_batch = static_cast< int >( value );
-		} else if( k == "packed_deep_rows" ) {
-			g_packed_deep_rows = value;
 		} else if( k == "packed_min_rows" ) {
 			g_packed_min_rows = value;
 		} else if( k == "persist_rows" ) {
@@ -613,6 +617,34 @@ int slab_mat_device_bytes( slab_mat_t A, uint64_t * bytes ) {
 		need( A, "slab_mat_device_bytes" );
 		need( bytes, "slab_mat_device_bytes" );
 		*bytes = A->sell.bytes() + ( A->transposed ? A->transposed->sell.bytes() : 0 );
+	} );
+}
+
+namespace {
+	void fill_format_info( const Sell & S, slab_format_info * out ) {
+		out->packed = S.packed.usable() ? 1 : 0;
+		out->width_class = S.packed.ncodes;
+		out->dict_size = S.packed.dict_size;
+		out->stride = S.packed.stride;
+		out->escaped_rows = S.packed.escaped_rows;
+		out->plain_bytes = S.bytes();
+		out->packed_bytes = S.packed_bytes();
+	}
+} // namespace
+
+int slab_mat_format_info( slab_mat_t A, slab_format_info * out ) {
+	return guarded( [ & ] {
+		need( A, "slab_mat_format_info" );
+		need( out, "slab_mat_format_info" );
+		fill_format_info( A->sell, out );
+	} );
+}
+
+int slab_level_format_info( slab_level_t level, slab_format_info * out ) {
+	return guarded( [ & ] {
+		need( level, "slab_level_format_info" );
+		need( out, "slab_level_format_info" );
+		fill_format_info( level->colorA, out );
 	} );
 }
 

@@ -67,7 +67,9 @@ namespace slabgpu {
 	extern int g_pack_build;   // build the dictionary-coded copy when a matrix is created
 	extern int g_packed_block; // threads per block of the packed kernels (tuning)
 	extern int g_packed_batch;
-	extern int64_t g_packed_deep_rows;
+	extern int g_packed_rows;
+	extern int g_packed_rows_spmv;
+	extern int64_t g_packed_multi_min_rows;
 	extern int64_t g_packed_min_rows;
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
@@ -99,6 +101,7 @@ namespace slabgpu {
 		DictEntry * h_dict = nullptr; // host copy: the kernels take the dictionary as a launch parameter
 		int dict_size = 0;         // entries in use, including entry 0
 		int64_t escaped_rows = 0;  // rows that fall back to the plain arrays
+		int stride = 0;            // slices between rows that mostly repeat their codes (0 = no such distance)
 		void release();
 		bool usable() const {
 			return codes != nullptr;

@@ -37,9 +37,14 @@ namespace slabgpu {
 	int g_use_packed = 1;
 	int g_pack_build = 1;
 	int g_packed_block = 256;
-	int g_packed_batch = 1;              // words (of 4 codes) gathered together by many-wave launches
-	int64_t g_packed_deep_rows = 0;      // launches below this many rows gather the whole row at once (measured:
-	                                     // never better than the short batches once the dictionary left shared memory)
+	// Tuning, all measured on B200 (tools/kernel_microbench.py, tools/solve_sweep.py):
+	// single-row kernels gather two 4-code words at a time (the launches they serve, 65k-300k rows, are
+	// latency-bound; one word at a time is better only for many-wave launches, which the multi-row kernels
+	// take; the whole row at once was never better once the dictionary left shared memory)
+	int g_packed_batch = 2;
+	int g_packed_rows = 2;               // rows per thread where rows repeat their codes at a fixed distance (1 = off):
+	int g_packed_rows_spmv = 3;          // ... colour steps / products (measured on B200, tools/kernel_microbench.py)
+	int64_t g_packed_multi_min_rows = 300000; // ... for launches of at least this many rows
 	int64_t g_packed_min_rows = 65536;   // launches below this many rows use the plain kernels (measured: their
 	                                     // matrices sit in the L2, where the plain preload shape is faster)
 
@@ -50,7 +55,7 @@ namespace slabgpu {
 		codes = nullptr;
 		dict = nullptr;
 		h_dict = nullptr;
-		max_width = ncodes = chunks = dict_size = 0;
+		max_width = ncodes = chunks = dict_size = stride = 0;
 		escaped_rows = 0;
 	}
 
@@ -438,18 +443,307 @@ namespace slabgpu {
 				}
 			}
 
+			// ------------------------------------------------------------ several rows per thread
+
+			// Rows that lie a fixed number of slices apart mostly carry the same codes (same place in the
+			// next grid line). A thread that owns R such rows decodes every code once and applies it to all
+			// of them: R times fewer constant-cache reads and decode instructions, R times more gathers in
+			// flight per thread, and the R rows re-read each other's neighbourhood while it is still in L1.
+			// The arithmetic of each row and its order are unchanged.
+			template< int CHUNKS >
+			__device__ __forceinline__ bool same_codes( const RowCodes< CHUNKS > & a, const RowCodes< CHUNKS > & b ) {
+				unsigned int diff = 0u;
+				#pragma unroll
+				for( int j = 0; j < CHUNKS; ++j ) {
+					diff |= ( a.q[ j ].x ^ b.q[ j ].x ) | ( a.q[ j ].y ^ b.q[ j ].y ) | ( a.q[ j ].z ^ b.q[ j ].z ) | ( a.q[ j ].w ^ b.q[ j ].w );
+				}
+				return diff == 0u;
+			}
+
+			template< int NCODES, int CHUNKS, int R, bool RAGGED, int DICT >
+			__device__ __forceinline__ void shared_rows_sum( const RowCodes< CHUNKS > & rc, const double * const ( &xrow )[ R ],
+				const DictParam< DICT > & dp, double ( &acc )[ R ] ) {
+				constexpr int WORDS = ( NCODES + 3 ) / 4;
+				#pragma unroll
+				for( int r = 0; r < R; ++r ) {
+					acc[ r ] = 0.0;
+				}
+				#pragma unroll
+				for( int wi = 0; wi < WORDS; ++wi ) {
+					const unsigned int word = rc.word( wi );
+					double v[ 4 ], xv[ R ][ 4 ];
+					int32_t dl[ 4 ];
+					#pragma unroll
+					for( int j = 0; j < 4; ++j ) {
+						if( 4 * wi + j < NCODES ) {
+							const unsigned int code = ( word >> ( 8 * j ) ) & 0xffu;
+							dl[ j ] = dp.delta[ code ];
+							v[ j ] = dp.val[ code ];
+						}
+					}
+					#pragma unroll
+					for( int r = 0; r < R; ++r ) {
+						#pragma unroll
+						for( int j = 0; j < 4; ++j ) {
+							if( 4 * wi + j < NCODES ) {
+								xv[ r ][ j ] = xrow[ r ][ dl[ j ] ];
+							}
+						}
+					}
+					#pragma unroll
+					for( int r = 0; r < R; ++r ) {
+						#pragma unroll
+						for( int j = 0; j < 4; ++j ) {
+							if( 4 * wi + j < NCODES ) {
+								const double sum = __dadd_rn( acc[ r ], __dmul_rn( v[ j ], xv[ r ][ j ] ) );
+								if( RAGGED ) {
+									acc[ r ] = ( ( word >> ( 8 * j ) ) & 0xffu ) != 0u ? sum : acc[ r ];
+								} else {
+									acc[ r ] = sum;
+								}
+							}
+						}
+					}
+				}
+			}
+
+			// position of row r of this thread: warp `gw` of the launch owns lane-columns of the slices
+			// first + tile*R*stride + j + r*stride, tile = gw / stride, j = gw % stride
+			template< int R >
+			__device__ __forceinline__ int64_t multi_slice( int64_t first_slice, int64_t gw, int stride, int r ) {
+				const int64_t tile = gw / stride;
+				const int64_t j = gw - tile * stride;
+				return first_slice + tile * ( static_cast< int64_t >( R ) * stride ) + j + static_cast< int64_t >( r ) * stride;
+			}
+
+			// k_gs_color_packed with R rows per thread; covers the contiguous range [pos_begin, pos_begin + pos_count)
+			template< int NCODES, int CHUNKS, int R, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
+				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
+				const int lane = threadIdx.x & 31;
+				const int64_t gw = ( static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x ) >> 5;
+				int32_t i[ R ];
+				int64_t pos[ R ];
+				RowCodes< CHUNKS > rc[ R ];
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					pos[ q ] = multi_slice< R >( pos_begin >> 5, gw, stride, q ) * kSlice + lane;
+					i[ q ] = -1;
+					#pragma unroll
+					for( int j = 0; j < CHUNKS; ++j ) {
+						rc[ q ].q[ j ] = make_uint4( 0u, 0u, 0u, 0u );
+					}
+					if( pos[ q ] < pos_begin + pos_count ) {
+						i[ q ] = rows != nullptr ? rows[ pos[ q ] ] : static_cast< int32_t >( pos[ q ] );
+						codes_load( codes, pos[ q ], rc[ q ] );
+					}
+				}
+				dep_trigger();
+				dep_wait();
+				bool same = i[ 0 ] >= 0 && !rc[ 0 ].escaped();
+				#pragma unroll
+				for( int q = 1; q < R; ++q ) {
+					same = same && i[ q ] >= 0 && same_codes( rc[ q ], rc[ 0 ] );
+				}
+				const bool shared = __all_sync( 0xffffffffu, same );
+				const bool warp_ragged = __any_sync( 0xffffffffu, rc[ 0 ].template ragged< NCODES >() );
+				if( shared ) {
+					double ri[ R ], zi[ R ], acc[ R ];
+					const double * zrow[ R ];
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						ri[ q ] = r[ i[ q ] ];
+						zi[ q ] = z[ i[ q ] ];
+						zrow[ q ] = z + i[ q ];
+						if( flags & 1 ) {
+							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ pos[ q ] - pos_begin ] ) );
+							zi[ q ] = __dadd_rn( __dmul_rn( 1.0, zi[ q ] ), __dmul_rn( 1.0, f ) );
+							z[ i[ q ] ] = zi[ q ];
+						}
+					}
+					const double d = dp.val[ rc[ 0 ].diag_code() ];
+					if( warp_ragged ) {
+						shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
+					} else {
+						shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
+					}
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						z[ i[ q ] ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri[ q ], -acc[ q ] ), __dmul_rn( zi[ q ], d ) ), d );
+					}
+					if( flags & 2 ) {
+						if( warp_ragged ) {
+							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
+						} else {
+							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
+						}
+						#pragma unroll
+						for( int q = 0; q < R; ++q ) {
+							const double f = __dadd_rn( __dmul_rn( 1.0, ri[ q ] ), __dmul_rn( -1.0, acc[ q ] ) );
+							out[ pos[ q ] - pos_begin ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+							zero[ pos[ q ] - pos_begin ] = 0.0;
+						}
+					}
+					return;
+				}
+				// rows that differ (grid boundaries, escaped rows, the tail of the range): one at a time
+				// (unrolled: indexing the per-row arrays with a run-time q would push them to local memory)
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					if( i[ q ] < 0 ) {
+						continue;
+					}
+					const int64_t coarse = pos[ q ] - pos_begin;
+					const double ri = r[ i[ q ] ];
+					double zi = z[ i[ q ] ];
+					if( flags & 1 ) {
+						const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ coarse ] ) );
+						zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+						z[ i[ q ] ] = zi;
+					}
+					double d = 0.0;
+					const double sum = any_row_sum< NCODES, CHUNKS, 1, true >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, d );
+					z[ i[ q ] ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
+					if( flags & 2 ) {
+						double unused = 0.0;
+						const double az = any_row_sum< NCODES, CHUNKS, 1, false >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, unused );
+						const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
+						out[ coarse ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+						zero[ coarse ] = 0.0;
+					}
+				}
+			}
+
+			// k_spmv_packed (unmasked) with R rows per thread
+			template< int NCODES, int CHUNKS, int R, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_spmv_packed_multi( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, int stride, const double * x, double * y, int64_t count,
+				double * dot_partials ) {
+				__shared__ double smem[ 32 ];
+				const int lane = threadIdx.x & 31;
+				const int64_t gw = ( static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x ) >> 5;
+				int64_t row[ R ];
+				bool live[ R ];
+				RowCodes< CHUNKS > rc[ R ];
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					row[ q ] = multi_slice< R >( 0, gw, stride, q ) * kSlice + lane;
+					live[ q ] = row[ q ] < count;
+					#pragma unroll
+					for( int j = 0; j < CHUNKS; ++j ) {
+						rc[ q ].q[ j ] = make_uint4( 0u, 0u, 0u, 0u );
+					}
+					if( live[ q ] ) {
+						codes_load( codes, row[ q ], rc[ q ] );
+					}
+				}
+				dep_trigger();
+				dep_wait();
+				bool same = live[ 0 ] && !rc[ 0 ].escaped();
+				#pragma unroll
+				for( int q = 1; q < R; ++q ) {
+					same = same && live[ q ] && same_codes( rc[ q ], rc[ 0 ] );
+				}
+				const bool shared = __all_sync( 0xffffffffu, same );
+				const bool warp_ragged = __any_sync( 0xffffffffu, rc[ 0 ].template ragged< NCODES >() );
+				double prod = 0.0;
+				if( shared ) {
+					double acc[ R ];
+					const double * xrow[ R ];
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						xrow[ q ] = x + row[ q ];
+					}
+					if( warp_ragged ) {
+						shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], xrow, dp, acc );
+					} else {
+						shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], xrow, dp, acc );
+					}
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						y[ row[ q ] ] = acc[ q ];
+						if( dot_partials != nullptr ) { // the thread's rows in ascending order
+							prod = __dadd_rn( prod, __dmul_rn( x[ row[ q ] ], acc[ q ] ) );
+						}
+					}
+				} else {
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						if( !live[ q ] ) {
+							continue;
+						}
+						double unused = 0.0;
+						const double acc = any_row_sum< NCODES, CHUNKS, 1, false >( rc[ q ], true, plain, row[ q ], static_cast< int32_t >( row[ q ] ), x, dp, unused );
+						y[ row[ q ] ] = acc;
+						if( dot_partials != nullptr ) {
+							prod = __dadd_rn( prod, __dmul_rn( x[ row[ q ] ], acc ) );
+						}
+					}
+				}
+				if( dot_partials != nullptr ) {
+					const double block_sum = block_tree_sum( prod, smem );
+					if( threadIdx.x == 0 ) {
+						dot_partials[ blockIdx.x ] = block_sum;
+					}
+				}
+			}
+
+			// how often do the rows `s` slices apart carry the same codes? votes[s], s = 1..kMaxStride, over a
+			// sample of the slices; votes[0] counts the sampled rows
+			constexpr int kMaxStride = 32;
+			__global__ void __launch_bounds__( kBlock ) k_stride_votes( const uint4 * __restrict__ codes, int chunks, int64_t nslices,
+				int sample_every, unsigned long long * votes ) {
+				__shared__ unsigned int local[ kMaxStride + 1 ];
+				for( int t = threadIdx.x; t <= kMaxStride; t += blockDim.x ) {
+					local[ t ] = 0u;
+				}
+				__syncthreads();
+				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const int64_t slice = ( k >> 5 ) * sample_every;
+				const int lane = static_cast< int >( k & 31 );
+				if( slice < nslices ) {
+					uint4 mine[ kMaxChunks ];
+					bool empty = true;
+					for( int j = 0; j < chunks; ++j ) {
+						mine[ j ] = codes[ ( slice * chunks + j ) * kSlice + lane ];
+						empty = empty && ( mine[ j ].x | mine[ j ].y | mine[ j ].z | mine[ j ].w ) == 0u;
+					}
+					if( !empty ) {
+						atomicAdd( &local[ 0 ], 1u );
+						for( int s = 1; s <= kMaxStride; ++s ) {
+							if( slice + s >= nslices ) {
+								break;
+							}
+							bool equal = true;
+							for( int j = 0; j < chunks; ++j ) {
+								const uint4 other = codes[ ( ( slice + s ) * chunks + j ) * kSlice + lane ];
+								equal = equal && other.x == mine[ j ].x && other.y == mine[ j ].y && other.z == mine[ j ].z && other.w == mine[ j ].w;
+							}
+							if( equal ) {
+								atomicAdd( &local[ s ], 1u );
+							}
+						}
+					}
+				}
+				__syncthreads();
+				for( int t = threadIdx.x; t <= kMaxStride; t += blockDim.x ) {
+					if( local[ t ] != 0u ) {
+						atomicAdd( votes + t, static_cast< unsigned long long >( local[ t ] ) );
+					}
+				}
+			}
+
 			// ------------------------------------------------------------ dispatch on the width class
 
-			// batch: words whose gathers are in flight together (`deep`: the whole row); dictionary capacity
-			// of the parameter block: 32 entries (384 bytes) when that is enough, else all 256 (3 KB)
+			// batch: words (of 4 codes) whose gathers are in flight together; dictionary capacity of the
+			// parameter block: 32 entries (384 bytes) when that is enough, else all 256 (3 KB)
 			template< int N, int D, class F >
-			void by_batch( bool deep, F && f ) {
+			void by_batch( F && f ) {
 				constexpr int C = ( N + 16 ) / 16;
 				constexpr int W = ( N + 3 ) / 4;
-				if( deep ) {
-					f( std::integral_constant< int, N >(), std::integral_constant< int, C >(), std::integral_constant< int, W >(),
-						std::integral_constant< int, D >() );
-				} else if( g_packed_batch >= 2 && W > 2 ) {
+				if( g_packed_batch >= 2 && W > 2 ) {
 					f( std::integral_constant< int, N >(), std::integral_constant< int, C >(), std::integral_constant< int, 2 >(),
 						std::integral_constant< int, D >() );
 				} else {
@@ -458,22 +752,22 @@ namespace slabgpu {
 				}
 			}
 			template< int D, class F >
-			void by_width( int ncodes, bool deep, F && f ) {
+			void by_width( int ncodes, F && f ) {
 				switch( ncodes ) {
-					case 8: by_batch< 8, D >( deep, f ); break;
-					case 16: by_batch< 16, D >( deep, f ); break;
-					case 27: by_batch< 27, D >( deep, f ); break;
-					case 32: by_batch< 32, D >( deep, f ); break;
-					case 64: by_batch< 64, D >( deep, f ); break;
+					case 8: by_batch< 8, D >( f ); break;
+					case 16: by_batch< 16, D >( f ); break;
+					case 27: by_batch< 27, D >( f ); break;
+					case 32: by_batch< 32, D >( f ); break;
+					case 64: by_batch< 64, D >( f ); break;
 					default: fail( SLAB_ERR_INTERNAL, "packed matrix with an unknown width class" );
 				}
 			}
 			template< class F >
-			void by_shape( const Packed & P, bool deep, F && f ) {
+			void by_shape( const Packed & P, F && f ) {
 				if( P.dict_size <= 32 ) {
-					by_width< 32 >( P.ncodes, deep, f );
+					by_width< 32 >( P.ncodes, f );
 				} else {
-					by_width< 256 >( P.ncodes, deep, f );
+					by_width< 256 >( P.ncodes, f );
 				}
 			}
 			template< int DICT >
@@ -486,12 +780,49 @@ namespace slabgpu {
 				return dp;
 			}
 
+			// rows per thread of the multi-row kernels
+			template< int D, class F >
+			void by_width_rows( int ncodes, int rows_per_thread, F && f ) {
+				const auto go = [ & ]( auto N ) {
+					constexpr int C = ( N.value + 16 ) / 16;
+					if( rows_per_thread >= 4 ) {
+						f( N, std::integral_constant< int, C >(), std::integral_constant< int, 4 >(), std::integral_constant< int, D >() );
+					} else if( rows_per_thread == 3 ) {
+						f( N, std::integral_constant< int, C >(), std::integral_constant< int, 3 >(), std::integral_constant< int, D >() );
+					} else {
+						f( N, std::integral_constant< int, C >(), std::integral_constant< int, 2 >(), std::integral_constant< int, D >() );
+					}
+				};
+				switch( ncodes ) {
+					case 8: go( std::integral_constant< int, 8 >() ); break;
+					case 16: go( std::integral_constant< int, 16 >() ); break;
+					case 27: go( std::integral_constant< int, 27 >() ); break;
+					case 32: go( std::integral_constant< int, 32 >() ); break;
+					case 64: go( std::integral_constant< int, 64 >() ); break;
+					default: fail( SLAB_ERR_INTERNAL, "packed matrix with an unknown width class" );
+				}
+			}
+			template< class F >
+			void by_shape_rows( const Packed & P, int rows_per_thread, F && f ) {
+				if( P.dict_size <= 32 ) {
+					by_width_rows< 32 >( P.ncodes, rows_per_thread, f );
+				} else {
+					by_width_rows< 256 >( P.ncodes, rows_per_thread, f );
+				}
+			}
+			bool multi_for( const Packed & P, int rows_per_thread, int64_t rows ) {
+				return rows_per_thread >= 2 && P.stride > 0 && rows >= g_packed_multi_min_rows;
+			}
+			// warps (and from them blocks) a multi-row launch over `nslices` slices needs
+			unsigned int multi_grid( int64_t nslices, int rows_per_thread, int stride, int block ) {
+				const int64_t tile = static_cast< int64_t >( rows_per_thread ) * stride;
+				const int64_t tiles = ( nslices + tile - 1 ) / tile;
+				const int64_t warps = tiles * stride;
+				return blocks_for( static_cast< uint64_t >( warps ) * 32u, block );
+			}
+
 			int block_size() {
 				return g_packed_block == 128 ? 128 : 256;
-			}
-			// launches of fewer rows than this are latency-bound: every gather of a row goes out at once
-			bool deep_for( int64_t rows ) {
-				return rows < g_packed_deep_rows;
 			}
 
 		} // namespace
@@ -501,8 +832,20 @@ namespace slabgpu {
 			const Packed & P = S.packed;
 			const PlainRef plain{ S.slice_off, S.vals, S.cols };
 			const int block = block_size();
+			if( members == nullptr && multi_for( P, g_packed_rows_spmv, count ) ) {
+				unsigned int grid = 0;
+				by_shape_rows( P, g_packed_rows_spmv, [ & ]( auto N, auto C, auto R, auto D ) {
+					grid = multi_grid( ( count + kSlice - 1 ) / kSlice, R.value, P.stride, block );
+					launch_pdl( k_spmv_packed_multi< N.value, C.value, R.value, D.value >, grid, block, st, P.codes,
+						dict_param< D.value >( P ), plain, P.stride, x, y, count, dot_out != nullptr ? dot_partials : nullptr );
+				} );
+				if( dot_out != nullptr ) {
+					sum_partials( st, dot_partials, grid, dot_out );
+				}
+				return;
+			}
 			const unsigned int grid = blocks_for( count, block );
-			by_shape( P, deep_for( count ), [ & ]( auto N, auto C, auto B, auto D ) {
+			by_shape( P, [ & ]( auto N, auto C, auto B, auto D ) {
 				const auto dp = dict_param< D.value >( P );
 				if( members != nullptr ) {
 					launch_pdl( k_spmv_packed< N.value, C.value, B.value, true, D.value >, grid, block, st, P.codes, dp, plain,
@@ -523,7 +866,15 @@ namespace slabgpu {
 			const Packed & P = S.packed;
 			const PlainRef plain{ S.slice_off, S.vals, S.cols };
 			const int block = block_size();
-			by_shape( P, deep_for( pos_count ), [ & ]( auto N, auto C, auto B, auto D ) {
+			if( pos_list == nullptr && skip == nullptr && ( pos_begin % kSlice ) == 0 && multi_for( P, g_packed_rows, pos_count ) ) {
+				by_shape_rows( P, g_packed_rows, [ & ]( auto N, auto C, auto R, auto D ) {
+					launch_pdl( k_gs_color_packed_multi< N.value, C.value, R.value, D.value >,
+						multi_grid( ( pos_count + kSlice - 1 ) / kSlice, R.value, P.stride, block ), block, st, P.codes,
+						dict_param< D.value >( P ), plain, rows, P.stride, pos_begin, pos_count, z, r, flags, src, out, zero );
+				} );
+				return;
+			}
+			by_shape( P, [ & ]( auto N, auto C, auto B, auto D ) {
 				launch_pdl( k_gs_color_packed< N.value, C.value, B.value, D.value >, blocks_for( pos_count, block ), block, st, P.codes,
 					dict_param< D.value >( P ), plain, rows, pos_begin, pos_count, z, r, flags, src, out, zero, pos_list, skip );
 			} );
@@ -534,7 +885,7 @@ namespace slabgpu {
 			const Packed & P = S.packed;
 			const PlainRef plain{ S.slice_off, S.vals, S.cols };
 			const int block = block_size();
-			by_shape( P, deep_for( n_coarse ), [ & ]( auto N, auto C, auto B, auto D ) {
+			by_shape( P, [ & ]( auto N, auto C, auto B, auto D ) {
 				launch_pdl( k_residual_restrict_packed< N.value, C.value, B.value, D.value >, blocks_for( n_coarse, block ), block, st,
 					P.codes, dict_param< D.value >( P ), plain, rows, n_coarse, z, r, r_c, zero );
 			} );
@@ -648,6 +999,31 @@ namespace slabgpu {
 		if( P.escaped_rows * 8 > S.nrows ) {
 			P.release();
 			return;
+		}
+		// the slice distance at which rows most often repeat their codes (multi-row kernels)
+		{
+			unsigned long long * d_votes = nullptr;
+			unsigned long long votes[ kMaxStride + 1 ] = { 0 };
+			const int sample_every = S.nslices > 4096 ? 8 : 1;
+			const int64_t sampled = ( S.nslices + sample_every - 1 ) / sample_every;
+			SLAB_CUDA( cudaMalloc( &d_votes, sizeof( votes ) ) );
+			SLAB_CUDA( cudaMemsetAsync( d_votes, 0, sizeof( votes ), st ) );
+			k_stride_votes<<< dev::blocks_for( sampled * kSlice ), dev::kBlock, 0, st >>>( P.codes, P.chunks, S.nslices, sample_every, d_votes );
+			count_launch();
+			const cudaError_t err = cudaMemcpyAsync( votes, d_votes, sizeof( votes ), cudaMemcpyDeviceToHost, st );
+			const cudaError_t err2 = cudaStreamSynchronize( st );
+			cudaFree( d_votes );
+			if( err != cudaSuccess || err2 != cudaSuccess ) {
+				P.release();
+				SLAB_CUDA( err != cudaSuccess ? err : err2 );
+			}
+			int best = 0;
+			for( int t = 1; t <= kMaxStride; ++t ) {
+				if( votes[ t ] > ( best ? votes[ best ] : 0ull ) ) {
+					best = t;
+				}
+			}
+			P.stride = ( best > 0 && votes[ best ] * 4 >= votes[ 0 ] * 3 ) ? best : 0; // at least 3 rows in 4 repeat
 		}
 		S.packed = P;
 	}

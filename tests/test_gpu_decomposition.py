@@ -14,6 +14,19 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["default-kernels", "packed-kernels"])
+def kernel_family(request, slab):
+    """Every case runs twice: with the default launch-size thresholds (these small boxes then use the plain
+    SELL kernels) and with the thresholds at zero, so that the dictionary-coded kernels run — ghost
+    columns, escaped rows, boundary position lists and skip flags included."""
+    packed = request.param == "packed-kernels"
+    slab.set_tuning("packed_min_rows", 0 if packed else 65536)
+    slab.set_tuning("packed_multi_min_rows", 0 if packed else 300000)
+    yield request.param
+    slab.set_tuning("packed_min_rows", 65536)
+    slab.set_tuning("packed_multi_min_rows", 300000)
+
+
 class World:
     def __init__(self, slab, grid, local_dims, levels):
         self.slab = slab
