@@ -107,6 +107,15 @@ def gs_step_bytes(dims):
     return (12 * stencil_nnz(dims) + 32 * n) / 8.0
 
 
+def gs_step_bytes_coded(dims, info):
+    """bytes ONE colour-step launch has to move when the level is dictionary-coded (packed.cu): per row of the
+    colour 16 B code words x chunks + 4 B row index + r + z in + z out (8 B each), and the gathered vector once
+    per sweep (n * 8 / 8 per step) — the SURVEY model with the 12 B/nnz matrix term replaced by the codes."""
+    n = dims[0] * dims[1] * dims[2]
+    chunks = (info["width_class"] + 16) // 16
+    return (n / 8.0) * (16 * chunks + 4 + 24) + n
+
+
 # ----------------------------------------------------------------------------- clocks
 
 
@@ -390,13 +399,26 @@ def main():
         gs_ms = ctx.timer_stop()
         per_launch_s = gs_ms * 1e-3 / (16 * reps)
         achieved = gs_step_bytes(dims) / per_launch_s / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_gs_color_batched<9,5> (finest-level colour step, smoother.hpp:60-72)",
+        info = h.format_info()
+        coded = bool(info["packed"]) and n // 8 >= 65536
+        kernel = ("k_gs_color_packed_multi<27,2,2,32>" if n // 8 >= 300000 else "k_gs_color_packed<27,2,2,32>") if coded \
+            else "k_gs_color_batched<9,5>"
+        roofline = {"bound": "hbm", "kernel": kernel + " (finest-level colour step, smoother.hpp:60-72)",
                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": measured_traffic(dims), "algorithmic_bytes_per_launch": gs_step_bytes(dims),
                     "us_per_launch": per_launch_s * 1e6, "launches_per_step": 32 * CG_ITERS,
                     "share_of_step": 32 * CG_ITERS * per_launch_s * 1e3 / ms_per_step, "peak_source": peak_src,
                     "how": "16 launches of one symmetric sweep timed alone with CUDA events on the library stream, "
-                           "10 repetitions after 3 warm-ups; traffic = dram bytes per launch from profiles/r01_ncu_gs_color_192.txt"}
+                           "10 repetitions after 3 warm-ups; traffic = dram bytes per launch from profiles/r01_ncu_gs_packed_192.txt "
+                           "(cold cache: the gathered vector comes from DRAM there, from L2 in the live run)"}
+        if coded:
+            fb = gs_step_bytes_coded(dims, info)
+            roofline["format"] = {
+                "matrix": "dictionary-coded SELL-32 (packed.cu): 1 B per stored entry instead of the 12 B the SURVEY "
+                          "model counts, decoded exactly; frac > 1 means the launch beats the HBM time of the 12 B/nnz model",
+                "width_class": info["width_class"], "dict_size": info["dict_size"], "escaped_rows": info["escaped_rows"],
+                "bytes_per_launch": fb, "achieved": fb / per_launch_s / 1e9, "frac": fb / per_launch_s / 1e9 / peak,
+                "bound_now": "L1/L2 gather path and instruction issue (profiles/r01_ncu_gs_packed_192.txt), not HBM"}
 
     line = {
         "metric": "hpcg_gflops", "value": main_run["gflops"], "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,

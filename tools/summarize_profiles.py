@@ -55,7 +55,9 @@ def launch_list(name, workload):
         fh.write("\n".join(out) + "\n")
 
 
-WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__m_xbar2l1tex_read_bytes.sum",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "idc__request_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -66,9 +68,13 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 def full_capture(rep, label, traffic_key, traffic):
     src = os.path.join(OUT, rep)
-    if not os.path.exists(src):
+    exported = src.replace(".ncu-rep", "_raw.csv")  # `ncu -i ... --page raw --csv` run on the GPU box (reports over
+    if os.path.exists(src):                          # 32 MB do not fit gpurun's return channel next to each other)
+        raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    elif os.path.exists(exported):
+        raw = open(exported).read()
+    else:
         return
-    raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
     out = [f"ncu --set full --clock-control none --import-source on ({rep}), cold cache (ncu default cache control)", ""]
@@ -98,8 +104,11 @@ def main():
     tpath = os.path.join(PROF, "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath))
-    full_capture("r01_prof_gs_192.ncu-rep", "r01_ncu_gs_color_192.txt", ("gs_color_step", "192x192x192"), traffic)
-    full_capture("r01_prof_spmv_192.ncu-rep", "r01_ncu_spmv_192.txt", ("spmv", "192x192x192"), traffic)
+    full_capture("r01_prof_gs_192.ncu-rep", "r01_ncu_gs_color_192.txt", ("gs_color_step_plain", "192x192x192"), traffic)
+    full_capture("r01_prof_spmv_192.ncu-rep", "r01_ncu_spmv_192.txt", ("spmv_plain", "192x192x192"), traffic)
+    # the dictionary-coded kernels (packed.cu): what bench.py's roofline.traffic reads
+    full_capture("r01_gs_packed_192.ncu-rep", "r01_ncu_gs_packed_192.txt", ("gs_color_step", "192x192x192"), traffic)
+    full_capture("r01_spmv_packed_192.ncu-rep", "r01_ncu_spmv_packed_192.txt", ("spmv", "192x192x192"), traffic)
     with open(tpath, "w") as fh:
         json.dump(traffic, fh, indent=1)
     print(json.dumps(traffic))
