@@ -402,10 +402,18 @@ namespace slabgpu {
 					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 					z[ i ] = zi;
 				}
-				double d = 0.0;
-				double s = chunk_accumulate< true >( rc, width < kChunk ? width : kChunk, z, 0.0, i, d );
-				s = row_tail< true >( vals, cols, begin, width, z, s, i, d );
-				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+				// flags & 4 — the step runs twice in a row (the last colour of the forward sweep is the first of the
+				//    backward sweep, smoother.hpp:108-111): nothing but z[i] itself changes in between, so the same
+				//    thread repeats the ordered row sum and the update with the matrix row still in registers.
+				const int passes = ( flags & 4 ) ? 2 : 1;
+				#pragma unroll 1
+				for( int pass = 0; pass < passes; ++pass ) {
+					double d = 0.0;
+					double s = chunk_accumulate< true >( rc, width < kChunk ? width : kChunk, z, 0.0, i, d );
+					s = row_tail< true >( vals, cols, begin, width, z, s, i, d );
+					zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+					z[ i ] = zi;
+				}
 				if( flags & 2 ) {
 					double unused = 0.0;
 					double az = chunk_accumulate< false >( rc, width < kChunk ? width : kChunk, z, 0.0, -1, unused );
@@ -1084,8 +1092,8 @@ namespace slabgpu {
 			const double * vals = S.vals;
 			const int32_t * cols = S.cols;
 			if( pos_count >= g_stream_rows ) {
-				if( flags & 2 ) {
-					fail( SLAB_ERR_INTERNAL, "gs_color_step: the streaming shape cannot fuse the residual" );
+				if( flags & 6 ) {
+					fail( SLAB_ERR_INTERNAL, "gs_color_step: the streaming shape cannot fuse the residual or repeat a step" );
 				}
 				const double * prolong = ( flags & 1 ) ? src : nullptr;
 				const unsigned int grid = blocks_for( pos_count );

@@ -38,8 +38,9 @@ namespace slabgpu {
 
 		// ---- fused Gauss-Seidel colour step (smoother.hpp:60-72) on the colour-major SELL
 		// flags bit 0: prolongation fused in front (z[i] += src[k], multigrid.hpp:71-81); bit 1: residual +
-		// restriction fused behind (out[k], zero[k] = 0; multigrid.hpp:100-104) — only where
-		// gs_color_step_can_fuse_residual(pos_count); both only on colour-0 steps of stencil levels.
+		// restriction fused behind (out[k], zero[k] = 0; multigrid.hpp:100-104); both only on colour-0 steps of
+		// stencil levels. Bit 2: the step is applied twice in a row (turnaround of a symmetric sweep,
+		// smoother.hpp:108-111). Bits 1 and 2 only where gs_color_step_can_fuse_residual(S, pos_count).
 		void gs_color_step( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags = 0,
 			const double * src = nullptr, double * out = nullptr, double * zero = nullptr, size_t window_bytes = 0,
 			const int32_t * pos_list = nullptr, const uint8_t * skip = nullptr );

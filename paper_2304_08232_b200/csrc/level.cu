@@ -390,10 +390,27 @@ namespace slabgpu {
 			}
 		}
 
+		// One forward + one backward sweep (smoother.hpp:108-111). The last colour of the forward sweep is the
+		// first of the backward sweep and nothing but its own entries changes in between, so on single-process
+		// levels that step is ONE launch whose threads apply the update twice (flags bit 2) — one launch and
+		// one pass over the colour's matrix rows less per symmetric sweep, same arithmetic in the same order.
+		// first_flags / last_flags ride on the first forward and the last backward step (grid transfers).
+		void sweep_pair_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, int first_flags = 0, int last_flags = 0 ) {
+			const uint64_t nc = L->num_colors;
+			const bool turnaround = L->ctx->fused_transfers && nc >= 2 && L->plan == nullptr
+				&& kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ nc - 1 ] ) );
+			for( uint64_t k = 0; k < nc; ++k ) {
+				const int flags = ( k == 0 ? first_flags : 0 ) | ( turnaround && k + 1 == nc ? 4 : 0 );
+				color_step_enqueue( L, k, z, r, flags );
+			}
+			for( uint64_t k = turnaround ? nc - 1 : nc; k > 0; --k ) {
+				color_step_enqueue( L, k - 1, z, r, k == 1 ? last_flags : 0 );
+			}
+		}
+
 		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) { // smoother.hpp:108-111
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				forward_enqueue( L, z, r );
-				backward_enqueue( L, z, r );
+				sweep_pair_enqueue( L, z, r );
 			}
 		}
 	} // namespace
@@ -716,11 +733,7 @@ namespace slabgpu {
 			const bool fuse_residual = kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ 0 ] ) );
 			const bool ghosts = L->z_c->n_alloc > L->z_c->n; // distributed: the ghost tail must be zeroed too
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				forward_enqueue( L, z, r );
-				for( uint64_t k = L->num_colors; k > 0; --k ) {
-					const bool last = sweep + 1 == sweeps && k == 1;
-					color_step_enqueue( L, k - 1, z, r, last && fuse_residual ? 2 : 0 );
-				}
+				sweep_pair_enqueue( L, z, r, 0, sweep + 1 == sweeps && fuse_residual ? 2 : 0 );
 			}
 			if( !fuse_residual ) {
 				kern::residual_restrict( ctx->stream, L->colorA, L->d_rows,
@@ -731,10 +744,7 @@ namespace slabgpu {
 			}
 			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				for( uint64_t k = 0; k < L->num_colors; ++k ) {
-					color_step_enqueue( L, k, z, r, sweep == 0 && k == 0 ? 1 : 0 );
-				}
-				backward_enqueue( L, z, r );
+				sweep_pair_enqueue( L, z, r, sweep == 0 ? 1 : 0, 0 );
 			}
 		}
 		if( count_stats ) {

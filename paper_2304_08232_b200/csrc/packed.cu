@@ -65,6 +65,11 @@ namespace slabgpu {
 
 			using namespace dev;
 
+// the two-rows-per-thread colour step at 4 resident blocks per SM (64 registers): +4 % over the
+// compiler's own 70; 5 blocks spill and lose 15 % (measured at 192^3)
+#ifndef GS_MULTI_MINBLOCKS
+#define GS_MULTI_MINBLOCKS 4
+#endif
 			constexpr int kDict = 256;
 			constexpr unsigned int kEscape = 255u;
 			constexpr int kMaxCodes = 64;
@@ -374,7 +379,7 @@ namespace slabgpu {
 			// smoother.hpp:60-72 fused, with the grid transfers of kernels.cu's k_gs_color riding on the
 			// colour-0 steps (flags bit 0: prolongation in front, bit 1: residual + restriction behind)
 			template< int NCODES, int CHUNKS, int BATCH, int DICT >
-			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed( const uint4 * __restrict__ codes,
+			__global__ void __launch_bounds__( kBlock, 4 ) k_gs_color_packed( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
 				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
@@ -403,9 +408,16 @@ namespace slabgpu {
 					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 					z[ i ] = zi;
 				}
-				double d = 0.0;
-				const double s = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, z, dp, d );
-				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+				// flags bit 2: the step runs twice in a row (the last colour of a forward sweep is the first of the
+				// backward sweep, smoother.hpp:108-111); nothing but z[i] itself changes in between
+				const int passes = ( flags & 4 ) ? 2 : 1;
+				#pragma unroll 1
+				for( int pass = 0; pass < passes; ++pass ) {
+					double d = 0.0;
+					const double s = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, z, dp, d );
+					zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
+					z[ i ] = zi;
+				}
 				if( flags & 2 ) {
 					double unused = 0.0;
 					const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, z, dp, unused );
@@ -518,7 +530,7 @@ namespace slabgpu {
 
 			// k_gs_color_packed with R rows per thread; covers the contiguous range [pos_begin, pos_begin + pos_count)
 			template< int NCODES, int CHUNKS, int R, int DICT >
-			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
+			__global__ void __launch_bounds__( kBlock, GS_MULTI_MINBLOCKS ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
 				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
@@ -564,14 +576,19 @@ namespace slabgpu {
 						}
 					}
 					const double d = dp.val[ rc[ 0 ].diag_code() ];
-					if( warp_ragged ) {
-						shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
-					} else {
-						shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
-					}
-					#pragma unroll
-					for( int q = 0; q < R; ++q ) {
-						z[ i[ q ] ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri[ q ], -acc[ q ] ), __dmul_rn( zi[ q ], d ) ), d );
+					const int passes = ( flags & 4 ) ? 2 : 1; // see k_gs_color_packed
+					#pragma unroll 1
+					for( int pass = 0; pass < passes; ++pass ) {
+						if( warp_ragged ) {
+							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
+						} else {
+							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
+						}
+						#pragma unroll
+						for( int q = 0; q < R; ++q ) {
+							zi[ q ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri[ q ], -acc[ q ] ), __dmul_rn( zi[ q ], d ) ), d );
+							z[ i[ q ] ] = zi[ q ];
+						}
 					}
 					if( flags & 2 ) {
 						if( warp_ragged ) {
@@ -603,9 +620,14 @@ namespace slabgpu {
 						zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
 						z[ i[ q ] ] = zi;
 					}
-					double d = 0.0;
-					const double sum = any_row_sum< NCODES, CHUNKS, 1, true >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, d );
-					z[ i[ q ] ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
+					const int passes = ( flags & 4 ) ? 2 : 1;
+					#pragma unroll 1
+					for( int pass = 0; pass < passes; ++pass ) {
+						double d = 0.0;
+						const double sum = any_row_sum< NCODES, CHUNKS, 1, true >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, d );
+						zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
+						z[ i[ q ] ] = zi;
+					}
 					if( flags & 2 ) {
 						double unused = 0.0;
 						const double az = any_row_sum< NCODES, CHUNKS, 1, false >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, unused );
