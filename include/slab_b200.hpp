@@ -232,6 +232,12 @@ namespace slab_b200 {
 			detail::check( slab_mat_shape( m_, nullptr, nullptr, &v ) );
 			return v;
 		}
+		// how the matrix is held on the device: plain SELL-32 only, or with the dictionary-coded copy
+		slab_format_info format_info() const {
+			slab_format_info info{};
+			detail::check( slab_mat_format_info( m_, &info ) );
+			return info;
+		}
 		slab_mat_t handle() const noexcept {
 			return m_;
 		}
@@ -424,6 +430,12 @@ namespace slab_b200 {
 			uint64_t v = 0;
 			detail::check( slab_level_color_info( h_, k, nullptr, &v ) );
 			return v;
+		}
+		// how the colour-major matrix copy the smoother reads is held on the device (slab_b200.h: slab_format_info)
+		slab_format_info format_info() const {
+			slab_format_info info{};
+			detail::check( slab_level_format_info( h_, &info ) );
+			return info;
 		}
 		LevelStats stats() const {
 			slab_level_stats s{};

@@ -156,31 +156,6 @@ namespace slabgpu {
 				return acc;
 			}
 
-			// Streaming form of the same ordered row sum for launches of many waves: a short rolling
-			// window of loads per thread (32 registers, 64 resident warps per SM) sustains more HBM
-			// bandwidth than the preload form, whose strength is the latency-bound small launch.
-			template< bool WANT_DIAG >
-			__device__ __forceinline__ double row_sum_streaming( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, int64_t pos, const double * x,
-				int32_t diag_row, double & diag ) {
-				const int64_t s = pos >> 5;
-				const int64_t begin = slice_off[ s ] + ( pos & 31 );
-				const int64_t end = slice_off[ s + 1 ];
-				double acc = 0.0;
-				#pragma unroll 9
-				for( int64_t e = begin; e < end; e += kSlice ) {
-					const int32_t c = __ldcs( cols + e );
-					const double v = __ldcs( vals + e );
-					const double xv = x[ c < 0 ? 0 : c ];
-					const double sum = __dadd_rn( acc, __dmul_rn( v, xv ) );
-					acc = c < 0 ? acc : sum;
-					if( WANT_DIAG ) {
-						diag = c == diag_row ? v : diag;
-					}
-				}
-				return acc;
-			}
-
 			// ------------------------------------------------------------ vector ops
 
 			__global__ void k_fill( double * __restrict__ v, uint64_t n, double value ) {
@@ -755,40 +730,6 @@ namespace slabgpu {
 			}
 
 			// ---- streaming forms (many-wave launches on the fine level); same arithmetic, same order
-
-			__global__ void __launch_bounds__( kBlock ) k_spmv_stream( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, int64_t nrows ) {
-				dep_trigger();
-				dep_wait();
-				const int64_t row = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( row >= nrows ) {
-					return;
-				}
-				double unused = 0.0;
-				y[ row ] = row_sum_streaming< false >( slice_off, vals, cols, row, x, -1, unused );
-			}
-
-			__global__ void __launch_bounds__( kBlock ) k_gs_color_stream( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r ) {
-				dep_trigger();
-				dep_wait();
-				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( k >= pos_count ) {
-					return;
-				}
-				const int64_t pos = pos_begin + k;
-				const int32_t i = rows[ pos ];
-				if( i < 0 ) {
-					return;
-				}
-				double d = 0.0;
-				const double s = row_sum_streaming< true >( slice_off, vals, cols, pos, z, i, d );
-				const double zi = z[ i ];
-				const double ri = r[ i ];
-				z[ i ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
-			}
 
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_stream( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,

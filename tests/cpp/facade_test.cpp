@@ -94,6 +94,9 @@ int main() {
 		rbgs_symmetric( level, direct, r );
 		CHECK( direct == composed );
 		CHECK( level.stats().nnz_visited == 4 * level.A().nnz() );
+		// the 27-point operator repeats at most 27 (offset, value) pairs: both copies are dictionary-coded
+		CHECK( level.format_info().packed == 1 && level.format_info().escaped_rows == 0 );
+		CHECK( level.A().format_info().packed == 1 && level.A().format_info().dict_size >= 2 && level.A().format_info().dict_size <= 28 );
 		CHECK_THROWS_AS( rbgs_symmetric( level, direct, r, SmootherConfig{ 0 } ), InvalidArgument );
 		DenseVector wrong( ctx, 3 );
 		CHECK_THROWS_AS( rbgs_forward( level, wrong, r ), DimensionMismatch );
