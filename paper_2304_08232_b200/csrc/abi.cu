@@ -159,14 +159,31 @@ int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, in
 		Sell PS = level->colorA;
 		PS.cols = pcols;
 		PS.packed = Packed();
-		if( g_use_packed ) {
-			sell_pack( ctx, PS, nullptr );
+		// one coded view per colour block: a colour's rows use at most as many pairs as a row has entries, so
+		// each view's dictionary fits the small parameter block
+		std::vector< Sell > views( level->num_colors );
+		int32_t * iota = nullptr;
+		{
+			std::vector< int32_t > h_iota( npos );
+			for( int64_t p = 0; p < npos; ++p ) h_iota[ p ] = static_cast< int32_t >( p );
+			SLAB_CUDA( cudaMalloc( &iota, std::max< int64_t >( npos, 1 ) * sizeof( int32_t ) ) );
+			upload_sync( st, iota, h_iota.data(), npos * sizeof( int32_t ) );
 		}
-		const bool packed = PS.packed.usable();
+		bool packed = g_use_packed != 0;
+		for( uint64_t k = 0; k < level->num_colors && packed; ++k ) {
+			Sell & V = views[ k ];
+			V = PS;
+			V.packed = Packed();
+			V.slice_off = PS.slice_off + level->color_pos[ k ] / kSlice;
+			V.nslices = ( level->color_pos[ k + 1 ] - level->color_pos[ k ] ) / kSlice;
+			V.nrows = V.nslices * kSlice;
+			sell_pack( ctx, V, iota + level->color_pos[ k ] );
+			packed = V.packed.usable();
+		}
 		const auto step = [ & ]( uint64_t k ) {
 			if( packed ) {
-				kern::gs_color_step_packed( st, PS, nullptr, level->color_pos[ k ], static_cast< int64_t >( level->color_size[ k ] ),
-					zp, rp, 0, nullptr, nullptr, nullptr, nullptr, nullptr );
+				kern::gs_color_step( st, views[ k ], iota + level->color_pos[ k ], 0, static_cast< int64_t >( level->color_size[ k ] ),
+					zp, rp );
 			} else {
 				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k ],
 					static_cast< int64_t >( level->color_size[ k ] ), zp, rp );
@@ -204,10 +221,13 @@ int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, in
 		SLAB_CUDA( cudaEventElapsedTime( &t, ctx->timer_start, ctx->timer_stop ) );
 		if( ms ) *ms = t / reps;
 		if( packed && max_diff ) {
-			std::fprintf( stderr, "position-space dictionary: %d entries, %lld escaped rows\n", PS.packed.dict_size,
-				static_cast< long long >( PS.packed.escaped_rows ) );
+			std::fprintf( stderr, "position-space dictionaries per colour: %d entries, %lld escaped rows, stride %d\n",
+				views[ 0 ].packed.dict_size, static_cast< long long >( views[ 0 ].packed.escaped_rows ), views[ 0 ].packed.stride );
 		}
-		PS.packed.release();
+		for( Sell & V : views ) {
+			V.packed.release();
+		}
+		cudaFree( iota );
 		cudaFree( nat2pos );
 		cudaFree( pcols );
 		cudaFree( zp );
