@@ -91,6 +91,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_use_packed = value ? 1 : 0;
 		} else if( k == "pack_build" ) {
 			g_pack_build = value ? 1 : 0;
+		} else if( k == "keep_plain" ) {
+			g_keep_plain = value ? 1 : 0;
 		} else if( k == "packed_block" ) {
 			g_packed_block = static_cast< int >( value );
 		} else if( k == "packed_rows" ) {
@@ -273,6 +275,9 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_PACKED" ) ) {
 			g_use_packed = std::atoi( v ) ? 1 : 0;
+		}
+		if( const char * v = std::getenv( "SLAB_KEEP_PLAIN" ) ) {
+			g_keep_plain = std::atoi( v ) ? 1 : 0;
 		}
 		if( const char * v = std::getenv( "SLAB_PACK_BUILD" ) ) {
 			g_pack_build = std::atoi( v ) ? 1 : 0;

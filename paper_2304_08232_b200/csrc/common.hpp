@@ -65,6 +65,7 @@ namespace slabgpu {
 	extern int g_use_pdl; // chain kernels with programmatic dependent launch (default on)
 	extern int g_use_packed;   // run products and colour steps from the dictionary-coded matrix copy when one exists
 	extern int g_pack_build;   // build the dictionary-coded copy when a matrix is created
+	extern int g_keep_plain;   // keep the plain arrays next to a coded copy without escaped rows (default 1)
 	extern int g_packed_block; // threads per block of the packed kernels (tuning)
 	extern int g_packed_batch;
 	extern int g_packed_rows;
@@ -118,8 +119,11 @@ namespace slabgpu {
 		double * vals = nullptr;       // device
 		int32_t * cols = nullptr;      // device, -1 = padding
 		void release();
+		bool plain_dropped() const { // the plain arrays were freed (g_keep_plain == 0): only the coded copy is left
+			return vals == nullptr && packed.usable();
+		}
 		uint64_t bytes() const {
-			return static_cast< uint64_t >( entries ) * 12u + static_cast< uint64_t >( nslices + 1 ) * 8u;
+			return ( plain_dropped() ? 0u : static_cast< uint64_t >( entries ) * 12u ) + static_cast< uint64_t >( nslices + 1 ) * 8u;
 		}
 		uint64_t packed_bytes() const {
 			return packed.usable() ? static_cast< uint64_t >( nslices ) * packed.chunks * kSlice * 16u + 256u * 16u : 0u;

@@ -289,6 +289,10 @@ namespace slabgpu {
 			std::memcpy( va, A->h_vals.data(), A->nnz * sizeof( double ) );
 			return;
 		}
+		if( A->sell.plain_dropped() ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "the matrix was created with keep_plain = 0: only its coded copy is on the device, "
+				"it cannot be downloaded or transposed" );
+		}
 		slab_ctx_s * ctx = A->ctx;
 		const int64_t nrows = static_cast< int64_t >( A->nrows );
 		int64_t * d_counts = nullptr;

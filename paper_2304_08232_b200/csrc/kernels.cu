@@ -945,7 +945,7 @@ namespace slabgpu {
 
 		namespace {
 			inline bool run_packed( const Sell & S, int64_t rows ) {
-				return g_use_packed && S.packed.usable() && rows >= g_packed_min_rows;
+				return S.plain_dropped() || ( g_use_packed && S.packed.usable() && rows >= g_packed_min_rows );
 			}
 		} // namespace
 

@@ -524,6 +524,11 @@ namespace slabgpu {
 			if( !L->is_stencil ) {
 				return false; // the fused transfers rely on "colour 0 == injected rows" and rows of <= 27 entries
 			}
+			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
+				if( at->colorA.plain_dropped() ) {
+					return false; // the persistent kernel reads the plain arrays
+				}
+			}
 			uint64_t largest = 0;
 			for( const uint64_t size : L->color_size ) {
 				largest = std::max( largest, size );

@@ -36,6 +36,10 @@ namespace slabgpu {
 
 	int g_use_packed = 1;
 	int g_pack_build = 1;
+	// keep the plain SELL arrays of a matrix whose coded copy has no escaped rows? 0 frees them (324 -> 32 bytes
+	// per 27-point row, i.e. 4-5x larger grids per GPU); such a matrix always runs the coded kernels and can no
+	// longer be downloaded or transposed. Set before the matrix is created.
+	int g_keep_plain = 1;
 	int g_packed_block = 256;
 	// Tuning, all measured on B200 (tools/kernel_microbench.py, tools/solve_sweep.py):
 	// single-row kernels gather two 4-code words at a time (the launches they serve, 65k-300k rows, are
@@ -1048,6 +1052,12 @@ namespace slabgpu {
 			P.stride = ( best > 0 && votes[ best ] * 4 >= votes[ 0 ] * 3 ) ? best : 0; // at least 3 rows in 4 repeat
 		}
 		S.packed = P;
+		if( !g_keep_plain && P.escaped_rows == 0 ) {
+			cudaFree( S.vals );
+			cudaFree( S.cols );
+			S.vals = nullptr;
+			S.cols = nullptr;
+		}
 	}
 
 } // namespace slabgpu

@@ -209,3 +209,30 @@ def test_pack_build_can_be_switched_off(slab, ctx, tune):
         assert h.format_info()["packed"] == 0 and h.A.format_info()["packed"] == 0
     finally:
         _capi.set_tuning("pack_build", 1)
+
+
+def test_plain_arrays_can_be_dropped(slab, ctx, tune):
+    """keep_plain = 0: matrices created afterwards keep only their coded copy (no escaped rows here), always
+    run the coded kernels — thresholds or not — and still reproduce the reference history bit for bit"""
+    import json
+    import os
+    from paper_2304_08232_b200 import _capi
+
+    ctx.dot_mode = slab.DOT_EXACT
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "history_16.json")))
+    _capi.set_tuning("keep_plain", 0)
+    try:
+        h = ctx.build_hierarchy((16, 16, 16), 4)
+    finally:
+        _capi.set_tuning("keep_plain", 1)
+    for info in (h.A.format_info(), h.format_info(), h.coarser.format_info()):
+        assert info["packed"] == 1 and info["plain_bytes"] < info["packed_bytes"]  # only the slice table is left
+    b = ctx.DenseVector(h.n())
+    slab.mxv(b, h.A, ctx.DenseVector(h.n(), 1.0))
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=50, fixed_iterations=50))
+    assert res.residual_history == gold["residual_history"]
+    with pytest.raises(slab.InvalidArgument):
+        h.A.csr()
+    kept = ctx.build_hierarchy((16, 16, 16), 1)  # created after the knob went back: plain arrays present
+    assert kept.A.format_info()["plain_bytes"] > kept.A.format_info()["packed_bytes"]
+    kept.A.csr()
