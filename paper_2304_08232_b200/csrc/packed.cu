@@ -14,10 +14,12 @@
 // plain kernels.
 //
 // With the stream 12x smaller, a fine-level colour step stops evicting the vector it gathers from the
-// L2; what bounds the kernels then is instruction issue and the L1/L2 gather path, so the decode is kept
-// to a handful of instructions per entry: one 16-byte shared-memory read yields value and offset, full
-// rows (no padding inside the width class) skip the per-entry padding test, and the diagonal a colour
-// step divides by is named by a spare byte of the row instead of being searched for.
+// L2; what bounds the kernels then is the L1 request path of the gathers, so everything else is kept off
+// it and the decode is a handful of instructions per entry: value and offset come from the dictionary
+// through indexed constant loads (the dictionary is a kernel parameter), full rows (no padding inside
+// the width class) skip the per-entry padding test, the diagonal a colour step divides by is named by a
+// spare byte of the row instead of being searched for, and many-wave launches give a thread several
+// rows that share their codes.
 #include "kernels.cuh"
 
 #include <algorithm>

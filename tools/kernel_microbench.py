@@ -69,7 +69,11 @@ def main():
             print("checksums match the reference bitwise:", ok, sums)
 
     runs = [("stream_variant=%d" % v) for v in args.variants] if args.sets is None else args.sets
+    defaults = {"packed": 1, "packed_block": 256, "packed_batch": 2, "packed_min_rows": 65536, "packed_rows": 2,
+                "packed_rows_spmv": 3, "packed_multi_min_rows": 300000, "stream_rows": 200000, "stream_variant": 2}
     for variant in runs:
+        for key, value in defaults.items():  # every set starts from the defaults
+            _capi.set_tuning(key, value)
         for pair in variant.split(","):
             key, value = pair.split("=")
             _capi.set_tuning(key, int(value))
