@@ -527,11 +527,12 @@ namespace slabgpu {
 
 			// position of row r of this thread: warp `gw` of the launch owns lane-columns of the slices
 			// first + tile*R*stride + j + r*stride, tile = gw / stride, j = gw % stride
+			// (32-bit arithmetic: a 64-bit division is a ~100-instruction subroutine, and every thread would run it)
 			template< int R >
-			__device__ __forceinline__ int64_t multi_slice( int64_t first_slice, int64_t gw, int stride, int r ) {
-				const int64_t tile = gw / stride;
-				const int64_t j = gw - tile * stride;
-				return first_slice + tile * ( static_cast< int64_t >( R ) * stride ) + j + static_cast< int64_t >( r ) * stride;
+			__device__ __forceinline__ int64_t multi_first_slice( int64_t first_slice, unsigned int gw, unsigned int stride ) {
+				const unsigned int tile = gw / stride;
+				const unsigned int j = gw - tile * stride;
+				return first_slice + static_cast< int64_t >( tile ) * ( R * stride ) + j;
 			}
 
 			// k_gs_color_packed with R rows per thread; covers the contiguous range [pos_begin, pos_begin + pos_count)
@@ -541,13 +542,14 @@ namespace slabgpu {
 				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
 				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
 				const int lane = threadIdx.x & 31;
-				const int64_t gw = ( static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x ) >> 5;
+				const unsigned int gw = ( blockIdx.x * blockDim.x + threadIdx.x ) >> 5;
+				const int64_t slice0 = multi_first_slice< R >( pos_begin >> 5, gw, static_cast< unsigned int >( stride ) );
 				int32_t i[ R ];
 				int64_t pos[ R ];
 				RowCodes< CHUNKS > rc[ R ];
 				#pragma unroll
 				for( int q = 0; q < R; ++q ) {
-					pos[ q ] = multi_slice< R >( pos_begin >> 5, gw, stride, q ) * kSlice + lane;
+					pos[ q ] = ( slice0 + static_cast< int64_t >( q ) * stride ) * kSlice + lane;
 					i[ q ] = -1;
 					#pragma unroll
 					for( int j = 0; j < CHUNKS; ++j ) {
@@ -651,13 +653,14 @@ namespace slabgpu {
 				double * dot_partials ) {
 				__shared__ double smem[ 32 ];
 				const int lane = threadIdx.x & 31;
-				const int64_t gw = ( static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x ) >> 5;
+				const unsigned int gw = ( blockIdx.x * blockDim.x + threadIdx.x ) >> 5;
+				const int64_t slice0 = multi_first_slice< R >( 0, gw, static_cast< unsigned int >( stride ) );
 				int64_t row[ R ];
 				bool live[ R ];
 				RowCodes< CHUNKS > rc[ R ];
 				#pragma unroll
 				for( int q = 0; q < R; ++q ) {
-					row[ q ] = multi_slice< R >( 0, gw, stride, q ) * kSlice + lane;
+					row[ q ] = ( slice0 + static_cast< int64_t >( q ) * stride ) * kSlice + lane;
 					live[ q ] = row[ q ] < count;
 					#pragma unroll
 					for( int j = 0; j < CHUNKS; ++j ) {
