@@ -59,6 +59,51 @@ def test_solution_and_history_match_oracle_bitwise(slab, ctx, oracle, n):
     assert np.array_equal(res.solution.values(), ores.solution)
 
 
+def test_full_size_104_history_matches_reference_golden(slab, ctx):
+    """BASELINE.json configs[3] at its real size (104^3 per GPU, 104 -> 52 -> 26 -> 13): the launches of this solve are
+    large enough for the dictionary-coded kernels (products with several rows per thread, fine-level colour steps from
+    the coded copy, fused transfers), the coarse levels run the plain ones. Exact-dot mode: the 51 residual norms and
+    the solution checksum equal the reference's doubles; tree-dot mode stays within 1e-10."""
+    gold = _golden("history_104.json")
+    h = ctx.build_hierarchy((104, 104, 104), 4)
+    assert h.format_info()["packed"] == 1 and h.A.format_info()["packed"] == 1
+    b = _rhs_A_ones(slab, ctx, h)
+    x0 = ctx.DenseVector(h.n(), 0.0)
+    cfg = slab.CGConfig(max_iters=50, fixed_iterations=50)
+    ctx.dot_mode = slab.DOT_EXACT
+    res = slab.cg_solve(h, b, x0, cfg)
+    assert res.iterations == 50
+    assert res.residual_history == gold["residual_history"]
+    assert slab.dot(res.solution, res.solution) == float.fromhex(gold["solution_checksum_dot_xx_hex"])
+    ctx.dot_mode = slab.DOT_TREE
+    tree = slab.cg_solve(h, b, x0, cfg)
+    want = np.array(gold["residual_history"])
+    assert np.max(np.abs(np.array(tree.residual_history) - want) / want) <= 1e-10
+    ctx.dot_mode = slab.DOT_EXACT
+
+
+def test_full_size_192_history_matches_reference_samples(slab, ctx):
+    """BASELINE.json configs[4] at its real size (192^3 per GPU): the reference's residual norms recorded in
+    BASELINE.md §4 (printed with 17 significant digits from the reference headers on the CPU) at iterations
+    0, 1, 2, 10, 20, 30, 40, 50. Exact-dot mode reproduces them bit for bit through the multi-row coded kernels;
+    tree-dot mode (what bench.py times) stays within 1e-10."""
+    samples = {0: 4249.7632875255531, 1: 1068.1384902268064, 2: 600.15828317887372, 10: 133.47356732130282,
+               20: 64.665305938692569, 30: 39.327576380963947, 40: 23.353504941453021, 50: 4.7224858011121835}
+    h = ctx.build_hierarchy((192, 192, 192), 4)
+    info = h.format_info()
+    assert info["packed"] == 1 and info["escaped_rows"] == 0 and info["stride"] == 3  # 96 rows per x-line and colour
+    b = _rhs_A_ones(slab, ctx, h)
+    x0 = ctx.DenseVector(h.n(), 0.0)
+    cfg = slab.CGConfig(max_iters=50, fixed_iterations=50)
+    ctx.dot_mode = slab.DOT_EXACT
+    res = slab.cg_solve(h, b, x0, cfg)
+    assert {k: res.residual_history[k] for k in samples} == samples
+    ctx.dot_mode = slab.DOT_TREE
+    tree = slab.cg_solve(h, b, x0, cfg)
+    assert max(abs(tree.residual_history[k] - v) / v for k, v in samples.items()) <= 1e-10
+    ctx.dot_mode = slab.DOT_EXACT
+
+
 def test_tree_dot_history_within_1e10_at_64(slab, ctx):
     """The fast (tree) dot re-associates the reductions; at 64^3 the reference history must still be
     matched to BASELINE.json's 1e-10 relative tolerance per iteration."""
