@@ -236,3 +236,32 @@ def test_plain_arrays_can_be_dropped(slab, ctx, tune):
     kept = ctx.build_hierarchy((16, 16, 16), 1)  # created after the knob went back: plain arrays present
     assert kept.A.format_info()["plain_bytes"] > kept.A.format_info()["packed_bytes"]
     kept.A.csr()
+
+
+def test_microbench_256_checksums_with_both_kernel_families(slab, ctx, tune):
+    """BASELINE.json configs[2] at its real size (256^3, one level): y = A*x for x ~ U(-1,1) from seed 0, then one
+    coloured symmetric sweep on r = b - A*x from z = 0 (b = A*1). The four checksums (the reference's 4096-chunk
+    ordered dot) equal the reference's doubles with the coded kernels (products with 3 rows per thread, colour
+    steps with 2, the sweep turnaround) and with the plain SELL kernels."""
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "micro_256.json")))
+    ctx.dot_mode = slab.DOT_EXACT
+    lvl = ctx.build_hierarchy((256, 256, 256), 1)
+    n = lvl.n()
+    x, _ = ctx.random_vector(n, 0)
+    b = ctx.DenseVector(n)
+    slab.mxv(b, lvl.A, ctx.DenseVector(n, 1.0))
+    for packed in (1, 0):
+        tune(packed=packed)
+        y = ctx.DenseVector(n)
+        slab.mxv(y, lvl.A, x)
+        r = ctx.DenseVector(n)
+        slab.waxpby(r, 1.0, b, -1.0, y)
+        z = ctx.DenseVector(n, 0.0)
+        slab.rbgs_symmetric(lvl, z, r)
+        got = {"dot_yy": slab.dot(y, y), "dot_xy": slab.dot(x, y), "dot_zz_after_symmetric": slab.dot(z, z),
+               "dot_rz_after_symmetric": slab.dot(r, z)}
+        for key, value in got.items():
+            assert value == float.fromhex(gold[key + "_hex"]), (key, packed)
