@@ -289,7 +289,8 @@ namespace slabgpu {
 	// packed.cu: build S.packed from the entries of S (d_rows: position -> row, nullptr = identity);
 	// leaves S.packed unusable when the matrix does not compress (rows wider than 64 entries, or
 	// too many rows with entries outside a 254-pair dictionary)
-	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows );
+	// owned_cols: columns from this index on are ghost slots (never offered to the dictionary); < 0: none
+	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows, int64_t owned_cols = -1 );
 	Decomp single_domain( uint64_t nx, uint64_t ny, uint64_t nz );
 
 	// ---- dist.cu (3D domain decomposition, halo exchange, allreduce)

@@ -254,7 +254,7 @@ namespace slabgpu {
 		}
 		A->nnz = nnz; // equals (3nx-2)(3ny-2)(3nz-2) on a single domain (problem.hpp:80-82)
 		A->sell = sell_stencil27( ctx, D, nullptr, static_cast< int64_t >( A->nrows ) );
-		sell_pack( ctx, A->sell, nullptr );
+		sell_pack( ctx, A->sell, nullptr, static_cast< int64_t >( A->ncols ) ); // columns >= ncols are ghost slots
 		return A.release();
 	}
 

@@ -180,7 +180,7 @@ namespace slabgpu {
 					L->color_pos[ k + 1 ] - L->color_pos[ k ], L->d_rows );
 			}
 			L->colorA = sell_stencil27( ctx, D, L->d_rows, npos );
-		sell_pack( ctx, L->colorA, L->d_rows );
+			sell_pack( ctx, L->colorA, L->d_rows, static_cast< int64_t >( L->n ) ); // columns >= n are ghost slots
 			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
 			uint64_t n_coarse = 0;
 			if( with_restriction ) {

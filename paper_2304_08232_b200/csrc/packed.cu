@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <type_traits>
@@ -100,7 +101,7 @@ namespace slabgpu {
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
 				int64_t npos, int64_t npadded, const DictEntry * __restrict__ dict, int dict_size, int chunks,
 				uint4 * __restrict__ codes, unsigned long long * escaped, unsigned long long * cand_key, unsigned int cand_cap,
-				double * cand_val, int32_t * cand_delta ) {
+				double * cand_val, int32_t * cand_delta, unsigned int * cand_hits, int32_t owned_cols ) {
 				__shared__ long long s_val[ kDict ];
 				__shared__ int32_t s_delta[ kDict ];
 				for( int t = threadIdx.x; t < dict_size; t += blockDim.x ) {
@@ -145,29 +146,37 @@ namespace slabgpu {
 						}
 						if( code == 0u ) {
 							escape = true;
+						}
+						// columns beyond the owned ones are ghost slots of a decomposed level: their offsets repeat
+						// nowhere, so they are never offered (they would only crowd the regular pairs out of the set)
+						if( code == 0u && c < owned_cols ) {
 							// offer the pair: open-addressing set keyed by a 64-bit mix of the pair. (Two different
 							// pairs with one key are vanishingly rare and only delay the second by a round.)
 							unsigned long long key = ( static_cast< unsigned long long >( bits ) * 0x9E3779B97F4A7C15ull )
 								^ ( static_cast< unsigned long long >( static_cast< uint32_t >( delta ) ) * 0xC2B2AE3D27D4EB4Full );
 							key |= 1ull;
 							unsigned int slot = static_cast< unsigned int >( ( key >> 20 ) % cand_cap );
-							for( unsigned int probe = 0; probe < 64u; ++probe ) {
+							bool listed = false;
+							for( unsigned int probe = 0; probe < 64u && !listed; ++probe ) {
 								const unsigned long long cur = reinterpret_cast< volatile unsigned long long * >( cand_key )[ slot ];
 								if( cur == key ) {
-									break;
-								}
-								if( cur == 0ull ) {
+									listed = true;
+								} else if( cur == 0ull ) {
 									const unsigned long long old = atomicCAS( cand_key + slot, 0ull, key );
 									if( old == 0ull ) {
 										cand_val[ slot ] = vals[ e ];
 										cand_delta[ slot ] = delta;
-										break;
 									}
-									if( old == key ) {
-										break;
-									}
+									listed = old == 0ull || old == key;
 								}
-								slot = slot + 1 == cand_cap ? 0u : slot + 1;
+								if( !listed ) {
+									slot = slot + 1 == cand_cap ? 0u : slot + 1;
+								}
+							}
+							// how common is the pair? counted on every 64th row: the dictionary takes the most frequent
+							// pairs first (the ghost columns of a decomposed level offer thousands of pairs that occur once)
+							if( listed && ( pos & 63 ) == 0 ) {
+								atomicAdd( cand_hits + slot, 1u );
 							}
 						}
 						#pragma unroll
@@ -926,7 +935,7 @@ namespace slabgpu {
 
 	// ---------------------------------------------------------------- building the packed copy
 
-	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows ) {
+	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows, int64_t owned_cols ) {
 		using namespace kern;
 		S.packed.release();
 		const int ncodes = width_class( S.max_width );
@@ -943,6 +952,7 @@ namespace slabgpu {
 		unsigned long long * d_cand_key = nullptr;
 		double * d_cand_val = nullptr;
 		int32_t * d_cand_delta = nullptr;
+		unsigned int * d_cand_hits = nullptr;
 		cudaStream_t st = ctx->stream;
 		try {
 			SLAB_CUDA( cudaMalloc( &P.codes, static_cast< size_t >( npadded ) * P.chunks * sizeof( uint4 ) ) );
@@ -951,6 +961,7 @@ namespace slabgpu {
 			SLAB_CUDA( cudaMalloc( &d_cand_key, kCandCap * sizeof( unsigned long long ) ) );
 			SLAB_CUDA( cudaMalloc( &d_cand_val, kCandCap * sizeof( double ) ) );
 			SLAB_CUDA( cudaMalloc( &d_cand_delta, kCandCap * sizeof( int32_t ) ) );
+			SLAB_CUDA( cudaMalloc( &d_cand_hits, kCandCap * sizeof( unsigned int ) ) );
 			std::vector< DictEntry > dict( kDict, DictEntry{ 0.0, 0, 0 } );
 			std::set< std::pair< int32_t, uint64_t > > known;
 			int dict_size = 1; // entry 0: padding
@@ -959,8 +970,10 @@ namespace slabgpu {
 				upload_sync( st, P.dict, dict.data(), kDict * sizeof( DictEntry ) );
 				SLAB_CUDA( cudaMemsetAsync( d_escaped, 0, sizeof( unsigned long long ), st ) );
 				SLAB_CUDA( cudaMemsetAsync( d_cand_key, 0, kCandCap * sizeof( unsigned long long ), st ) );
+				SLAB_CUDA( cudaMemsetAsync( d_cand_hits, 0, kCandCap * sizeof( unsigned int ), st ) );
 				k_pack_rows<<< dev::blocks_for( npadded ), dev::kBlock, 0, st >>>( S.slice_off, S.vals, S.cols, d_rows, S.nrows, npadded,
-					P.dict, dict_size, P.chunks, P.codes, d_escaped, d_cand_key, kCandCap, d_cand_val, d_cand_delta );
+					P.dict, dict_size, P.chunks, P.codes, d_escaped, d_cand_key, kCandCap, d_cand_val, d_cand_delta, d_cand_hits,
+					static_cast< int32_t >( owned_cols < 0 || owned_cols > 0x7fffffff ? 0x7fffffff : owned_cols ) );
 				SLAB_CUDA( cudaGetLastError() );
 				count_launch();
 				SLAB_CUDA( cudaMemcpyAsync( &escaped, d_escaped, sizeof( escaped ), cudaMemcpyDeviceToHost, st ) );
@@ -971,19 +984,22 @@ namespace slabgpu {
 				std::vector< unsigned long long > ck( kCandCap );
 				std::vector< double > cv( kCandCap );
 				std::vector< int32_t > cd( kCandCap );
+				std::vector< unsigned int > ch( kCandCap );
+				SLAB_CUDA( cudaMemcpyAsync( ch.data(), d_cand_hits, kCandCap * sizeof( unsigned int ), cudaMemcpyDeviceToHost, st ) );
 				SLAB_CUDA( cudaMemcpyAsync( ck.data(), d_cand_key, kCandCap * sizeof( unsigned long long ), cudaMemcpyDeviceToHost, st ) );
 				SLAB_CUDA( cudaMemcpyAsync( cv.data(), d_cand_val, kCandCap * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
 				SLAB_CUDA( cudaMemcpyAsync( cd.data(), d_cand_delta, kCandCap * sizeof( int32_t ), cudaMemcpyDeviceToHost, st ) );
 				SLAB_CUDA( cudaStreamSynchronize( st ) );
-				// new pairs in a reproducible order (the set is filled in arrival order): narrow bands first,
-				// so that when the dictionary cannot hold everything the far-away columns (ghost slots of a
-				// decomposed level) are the ones left to the plain path
-				const auto band_order = []( const std::pair< int32_t, uint64_t > & a, const std::pair< int32_t, uint64_t > & b ) {
-					const int64_t da = a.first < 0 ? -static_cast< int64_t >( a.first ) : a.first;
-					const int64_t db = b.first < 0 ? -static_cast< int64_t >( b.first ) : b.first;
-					return da != db ? da < db : a < b;
+				// new pairs, the most frequent first (then narrow bands first, for a reproducible order): when the
+				// dictionary cannot hold everything, the pairs that occur once (ghost slots of a decomposed level)
+				// are the ones left to the plain path
+				struct Fresh {
+					unsigned int hits;
+					int32_t delta;
+					uint64_t bits;
 				};
-				std::set< std::pair< int32_t, uint64_t >, decltype( band_order ) > fresh( band_order );
+				std::vector< Fresh > fresh;
+				std::set< std::pair< int32_t, uint64_t > > seen;
 				for( unsigned int t = 0; t < kCandCap; ++t ) {
 					if( ck[ t ] == 0ull ) {
 						continue;
@@ -991,18 +1007,26 @@ namespace slabgpu {
 					uint64_t bits;
 					std::memcpy( &bits, &cv[ t ], sizeof( bits ) );
 					const std::pair< int32_t, uint64_t > key( cd[ t ], bits );
-					if( !known.count( key ) ) {
-						fresh.insert( key );
+					if( !known.count( key ) && seen.insert( key ).second ) {
+						fresh.push_back( Fresh{ ch[ t ], cd[ t ], bits } );
 					}
 				}
+				std::sort( fresh.begin(), fresh.end(), []( const Fresh & a, const Fresh & b ) {
+					if( a.hits != b.hits ) {
+						return a.hits > b.hits;
+					}
+					const int64_t da = a.delta < 0 ? -static_cast< int64_t >( a.delta ) : a.delta;
+					const int64_t db = b.delta < 0 ? -static_cast< int64_t >( b.delta ) : b.delta;
+					return da != db ? da < db : ( a.delta != b.delta ? a.delta < b.delta : a.bits < b.bits );
+				} );
 				bool grew = false;
-				for( const auto & key : fresh ) {
+				for( const Fresh & f : fresh ) {
 					if( dict_size >= kDict - 1 ) {
 						break;
 					}
-					known.insert( key );
-					dict[ dict_size ].delta = key.first;
-					std::memcpy( &dict[ dict_size ].val, &key.second, sizeof( double ) );
+					known.insert( std::make_pair( f.delta, f.bits ) );
+					dict[ dict_size ].delta = f.delta;
+					std::memcpy( &dict[ dict_size ].val, &f.bits, sizeof( double ) );
 					++dict_size;
 					grew = true;
 				}
@@ -1019,6 +1043,7 @@ namespace slabgpu {
 			cudaFree( d_cand_key );
 			cudaFree( d_cand_val );
 			cudaFree( d_cand_delta );
+			cudaFree( d_cand_hits );
 			P.release();
 			throw;
 		}
@@ -1026,6 +1051,11 @@ namespace slabgpu {
 		cudaFree( d_cand_key );
 		cudaFree( d_cand_val );
 		cudaFree( d_cand_delta );
+		cudaFree( d_cand_hits );
+		if( std::getenv( "SLAB_PACK_DEBUG" ) ) {
+			std::fprintf( stderr, "sell_pack: nrows %lld max_width %d dict %d escaped %lld\n", static_cast< long long >( S.nrows ),
+				S.max_width, P.dict_size, static_cast< long long >( P.escaped_rows ) );
+		}
 		// not worth it when many rows would take the plain path anyway (each costs both code paths)
 		if( P.escaped_rows * 8 > S.nrows ) {
 			P.release();

@@ -279,3 +279,16 @@ def test_single_rank_nccl_communicator_is_transparent(slab, ctx):
     assert got.residual_history == want.residual_history
     assert np.array_equal(got.solution.values(), want.solution.values())
     assert slab.dot(db, db) == slab.dot(b, b)
+
+
+def test_full_size_two_rank_vcycle_equals_global_bitwise(slab, ctx):
+    """BASELINE.json configs[3] on its 2x1x1 process grid at the real size: two ranks of 104^3 (global 208x104x104,
+    4 levels down to 13^3 per rank) in lockstep on one device. The fine-level launches are large enough for the
+    dictionary-coded kernels by themselves; rows next to the cut carry ghost columns outside the dictionary and are
+    read from the plain arrays; boundary rows run first from a position list, interior rows with skip flags."""
+    rank0 = slab.Context(0)
+    rank0.set_process_grid((2, 1, 1), 0)
+    info = rank0.build_hierarchy((104, 104, 104), 1).format_info()
+    # the x = 103 face looks across the cut: its rows (104 x 104, in four of the eight colours) cannot all be coded
+    assert info["packed"] == 1 and 0 < info["escaped_rows"] <= 104 * 104
+    _vcycle_case(slab, ctx, (2, 1, 1), (104, 104, 104), 4)
