@@ -292,3 +292,11 @@ def test_full_size_two_rank_vcycle_equals_global_bitwise(slab, ctx):
     # the x = 103 face looks across the cut: its rows (104 x 104, in four of the eight colours) cannot all be coded
     assert info["packed"] == 1 and 0 < info["escaped_rows"] <= 104 * 104
     _vcycle_case(slab, ctx, (2, 1, 1), (104, 104, 104), 4)
+
+
+def test_full_size_eight_rank_vcycle_equals_global_bitwise(slab, ctx, kernel_family):
+    """BASELINE.json configs[3] on its 2x2x2 process grid at the real size: eight ranks of 104^3 (global 208^3,
+    4 levels, odd 13^3 boxes with odd offsets at the coarsest level) in lockstep on one device."""
+    if kernel_family != "default-kernels":
+        pytest.skip("one pass at this size is enough: the default thresholds already select the coded kernels")
+    _vcycle_case(slab, ctx, (2, 2, 2), (104, 104, 104), 4)
