@@ -343,7 +343,9 @@ def main():
         return run_reference_arm(args, dims)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    # SLAB_BENCH_DISTRIBUTED=1 runs the multi-rank arm with a single rank (torchrun --nproc-per-node 1): the
+    # rendezvous, the NCCL communicator and the library's exchange/allreduce calls on a 1x1x1 process grid
+    if world > 1 or args.gpus > 1 or os.environ.get("SLAB_BENCH_DISTRIBUTED") == "1":
         from paper_2304_08232_b200 import distributed_bench
 
         return distributed_bench.main(args, dims)

@@ -139,7 +139,10 @@ def main(args, dims) -> int:
                     "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": int(launches),
             "halo_exchanges_per_rank": info["exchanges"],
-            "roofline": {"bound": "hbm", "kernel": "k_gs_color_batched (finest level colour step, includes its halo exchange)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("k_gs_color_packed* (coded copy)" if h.format_info()["packed"] else "k_gs_color_batched")
+                         + " — finest-level colour step of rank 0, including its halo exchange",
+                         "format": h.format_info(),
                          "achieved": bench.gs_step_bytes(dims) / per_launch_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": bench.gs_step_bytes(dims) / per_launch_s / 1e9 / peak, "traffic": bench.measured_traffic(dims),
                          "peak_source": peak_src},
