@@ -655,6 +655,146 @@ namespace slabgpu {
 				}
 			}
 
+			// k_gs_color_packed_multi for the interior launch of a colour on a decomposed level (skip flags)
+			template< int NCODES, int CHUNKS, int R, int DICT >
+			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed_multi_skip( const uint4 * __restrict__ codes,
+				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
+				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				const uint8_t * __restrict__ skip ) {
+				// skip: positions flagged here are left out (the interior launch of a colour on a decomposed level,
+				// whose boundary rows went first); such rows — like the padding at the end of the range — take part in
+				// the shared decode as passengers: they borrow a live row's codes and address and store nothing
+				const int lane = threadIdx.x & 31;
+				const unsigned int gw = ( blockIdx.x * blockDim.x + threadIdx.x ) >> 5;
+				const int64_t slice0 = multi_first_slice< R >( pos_begin >> 5, gw, static_cast< unsigned int >( stride ) );
+				int32_t i[ R ];
+				int64_t pos[ R ];
+				RowCodes< CHUNKS > rc[ R ];
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					pos[ q ] = ( slice0 + static_cast< int64_t >( q ) * stride ) * kSlice + lane;
+					i[ q ] = -1;
+					#pragma unroll
+					for( int j = 0; j < CHUNKS; ++j ) {
+						rc[ q ].q[ j ] = make_uint4( 0u, 0u, 0u, 0u );
+					}
+					if( pos[ q ] < pos_begin + pos_count && !( skip != nullptr && skip[ pos[ q ] ] ) ) {
+						i[ q ] = rows != nullptr ? rows[ pos[ q ] ] : static_cast< int32_t >( pos[ q ] );
+						if( i[ q ] >= 0 ) {
+							codes_load( codes, pos[ q ], rc[ q ] );
+						}
+					}
+				}
+				dep_trigger();
+				dep_wait();
+				// the lane's leader: its first live row (none: an idle lane with all-padding codes)
+				int lead = -1;
+				#pragma unroll
+				for( int q = R - 1; q >= 0; --q ) {
+					lead = i[ q ] >= 0 ? q : lead;
+				}
+				RowCodes< CHUNKS > lc = rc[ 0 ];
+				int32_t li = 0;
+				#pragma unroll
+				for( int q = 1; q < R; ++q ) {
+					if( lead == q ) {
+						lc = rc[ q ];
+					}
+				}
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					li = lead == q ? i[ q ] : li;
+				}
+				bool same = lead < 0 || !lc.escaped();
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					same = same && ( i[ q ] < 0 || same_codes( rc[ q ], lc ) );
+				}
+				const bool shared = __all_sync( 0xffffffffu, same );
+				const bool warp_ragged = __any_sync( 0xffffffffu, lc.template ragged< NCODES >() );
+				if( shared ) {
+					double ri[ R ], zi[ R ], acc[ R ];
+					const double * zrow[ R ];
+					#pragma unroll
+					for( int q = 0; q < R; ++q ) {
+						const int32_t at = i[ q ] >= 0 ? i[ q ] : li; // passengers read the leader's row (row 0 on idle lanes)
+						ri[ q ] = r[ at ];
+						zi[ q ] = z[ at ];
+						zrow[ q ] = z + at;
+						if( ( flags & 1 ) && i[ q ] >= 0 ) {
+							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ pos[ q ] - pos_begin ] ) );
+							zi[ q ] = __dadd_rn( __dmul_rn( 1.0, zi[ q ] ), __dmul_rn( 1.0, f ) );
+							z[ i[ q ] ] = zi[ q ];
+						}
+					}
+					const double d = dp.val[ lc.diag_code() ];
+					const int passes = ( flags & 4 ) ? 2 : 1; // see k_gs_color_packed
+					#pragma unroll 1
+					for( int pass = 0; pass < passes; ++pass ) {
+						if( warp_ragged ) {
+							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, zrow, dp, acc );
+						} else {
+							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, zrow, dp, acc );
+						}
+						#pragma unroll
+						for( int q = 0; q < R; ++q ) {
+							zi[ q ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri[ q ], -acc[ q ] ), __dmul_rn( zi[ q ], d ) ), d );
+							if( i[ q ] >= 0 ) {
+								z[ i[ q ] ] = zi[ q ];
+							}
+						}
+					}
+					if( flags & 2 ) {
+						if( warp_ragged ) {
+							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, zrow, dp, acc );
+						} else {
+							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, zrow, dp, acc );
+						}
+						#pragma unroll
+						for( int q = 0; q < R; ++q ) {
+							if( i[ q ] >= 0 ) {
+								const double f = __dadd_rn( __dmul_rn( 1.0, ri[ q ] ), __dmul_rn( -1.0, acc[ q ] ) );
+								out[ pos[ q ] - pos_begin ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+								zero[ pos[ q ] - pos_begin ] = 0.0;
+							}
+						}
+					}
+					return;
+				}
+				// rows that differ (grid boundaries, escaped rows, the tail of the range): one at a time
+				// (unrolled: indexing the per-row arrays with a run-time q would push them to local memory)
+				#pragma unroll
+				for( int q = 0; q < R; ++q ) {
+					if( i[ q ] < 0 ) {
+						continue;
+					}
+					const int64_t coarse = pos[ q ] - pos_begin;
+					const double ri = r[ i[ q ] ];
+					double zi = z[ i[ q ] ];
+					if( flags & 1 ) {
+						const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ coarse ] ) );
+						zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
+						z[ i[ q ] ] = zi;
+					}
+					const int passes = ( flags & 4 ) ? 2 : 1;
+					#pragma unroll 1
+					for( int pass = 0; pass < passes; ++pass ) {
+						double d = 0.0;
+						const double sum = any_row_sum< NCODES, CHUNKS, 1, true >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, d );
+						zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
+						z[ i[ q ] ] = zi;
+					}
+					if( flags & 2 ) {
+						double unused = 0.0;
+						const double az = any_row_sum< NCODES, CHUNKS, 1, false >( rc[ q ], true, plain, pos[ q ], i[ q ], z, dp, unused );
+						const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
+						out[ coarse ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
+						zero[ coarse ] = 0.0;
+					}
+				}
+			}
+
 			// k_spmv_packed (unmasked) with R rows per thread
 			template< int NCODES, int CHUNKS, int R, int DICT >
 			__global__ void __launch_bounds__( kBlock ) k_spmv_packed_multi( const uint4 * __restrict__ codes,
@@ -906,6 +1046,14 @@ namespace slabgpu {
 			const Packed & P = S.packed;
 			const PlainRef plain{ S.slice_off, S.vals, S.cols };
 			const int block = block_size();
+			if( pos_list == nullptr && skip != nullptr && ( pos_begin % kSlice ) == 0 && multi_for( P, g_packed_rows, pos_count ) ) {
+				by_shape_rows( P, g_packed_rows, [ & ]( auto N, auto C, auto R, auto D ) {
+					launch_pdl( k_gs_color_packed_multi_skip< N.value, C.value, R.value, D.value >,
+						multi_grid( ( pos_count + kSlice - 1 ) / kSlice, R.value, P.stride, block ), block, st, P.codes,
+						dict_param< D.value >( P ), plain, rows, P.stride, pos_begin, pos_count, z, r, flags, src, out, zero, skip );
+				} );
+				return;
+			}
 			if( pos_list == nullptr && skip == nullptr && ( pos_begin % kSlice ) == 0 && multi_for( P, g_packed_rows, pos_count ) ) {
 				by_shape_rows( P, g_packed_rows, [ & ]( auto N, auto C, auto R, auto D ) {
 					launch_pdl( k_gs_color_packed_multi< N.value, C.value, R.value, D.value >,
