@@ -183,6 +183,10 @@ int slab_level_stats_reset( slab_level_t level ); /* reset_stats problem.hpp:271
 
 /* ------------------------------------------------------------------ smoother (smoother.hpp) */
 int slab_rbgs_color_step( slab_level_t level, uint64_t k, slab_vec_t z, slab_vec_t r ); /* rbgs_color_step :60-72, fused */
+/* the same step twice in a row as ONE launch — what rbgs_symmetric does at the turnaround between its forward and
+ * backward sweep (:108-111: the last colour runs twice). Bit-identical to two calls of slab_rbgs_color_step; on a
+ * decomposed level the colour's halo message goes out once, after the second update. */
+int slab_rbgs_color_step_twice( slab_level_t level, uint64_t k, slab_vec_t z, slab_vec_t r );
 int slab_rbgs_forward( slab_level_t level, slab_vec_t z, slab_vec_t r );               /* :77-85 */
 int slab_rbgs_backward( slab_level_t level, slab_vec_t z, slab_vec_t r );              /* :92-100 */
 int slab_rbgs_symmetric( slab_level_t level, slab_vec_t z, slab_vec_t r, uint64_t sweeps ); /* :103-113 */

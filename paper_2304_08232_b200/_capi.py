@@ -155,6 +155,7 @@ SIGNATURES = {
     "slab_level_stats_get": (C.c_int, [_vp, C.POINTER(_LevelStats)]),
     "slab_level_stats_reset": (C.c_int, [_vp]),
     "slab_rbgs_color_step": (C.c_int, [_vp, _u64, _vp, _vp]),
+    "slab_rbgs_color_step_twice": (C.c_int, [_vp, _u64, _vp, _vp]),
     "slab_rbgs_forward": (C.c_int, [_vp, _vp, _vp]),
     "slab_rbgs_backward": (C.c_int, [_vp, _vp, _vp]),
     "slab_rbgs_symmetric": (C.c_int, [_vp, _vp, _vp, _u64]),
@@ -713,6 +714,12 @@ class SmootherConfig:  # smoother.hpp:48-50
 
 def rbgs_color_step(level: ProblemLevel, k: int, z: DenseVector, r: DenseVector) -> DenseVector:
     _check(_lib.slab_rbgs_color_step(level._h, int(k), z._h, r._h))
+    return z
+
+
+def rbgs_color_step_twice(level: ProblemLevel, k: int, z: DenseVector, r: DenseVector) -> DenseVector:
+    """the turnaround of a symmetric sweep: colour k updated twice in a row by one launch"""
+    _check(_lib.slab_rbgs_color_step_twice(level._h, int(k), z._h, r._h))
     return z
 
 

@@ -911,6 +911,13 @@ int slab_rbgs_color_step( slab_level_t level, uint64_t k, slab_vec_t z, slab_vec
 	} );
 }
 
+int slab_rbgs_color_step_twice( slab_level_t level, uint64_t k, slab_vec_t z, slab_vec_t r ) {
+	return guarded( [ & ] {
+		SLAB_LEVEL_ZR( "rbgs_color_step_twice" );
+		rbgs_color_step_twice( level, k, z, r );
+	} );
+}
+
 int slab_rbgs_forward( slab_level_t level, slab_vec_t z, slab_vec_t r ) {
 	return guarded( [ & ] {
 		SLAB_LEVEL_ZR( "rbgs_forward" );

@@ -321,6 +321,7 @@ namespace slabgpu {
 	slab_level_s * level_from_csr( slab_ctx_s * ctx, uint64_t n, const uint64_t * ro, const uint64_t * co,
 		const double * va );
 	void rbgs_color_step( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r );
+	void rbgs_color_step_twice( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r );
 	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r );
 	void rbgs_backward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r );
 	void rbgs_symmetric( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );

@@ -391,13 +391,15 @@ namespace slabgpu {
 		}
 
 		// One forward + one backward sweep (smoother.hpp:108-111). The last colour of the forward sweep is the
-		// first of the backward sweep and nothing but its own entries changes in between, so on single-process
-		// levels that step is ONE launch whose threads apply the update twice (flags bit 2) — one launch and
-		// one pass over the colour's matrix rows less per symmetric sweep, same arithmetic in the same order.
+		// first of the backward sweep and nothing but its own entries changes in between, so that step is ONE
+		// launch whose threads apply the update twice (flags bit 2) — one launch and one pass over the colour's
+		// matrix rows less per symmetric sweep, same arithmetic in the same order. On a decomposed level the
+		// halo message of that colour goes out once, after the second update: the rows of a colour never read
+		// the colour's own ghost copies, so nobody misses the intermediate values.
 		// first_flags / last_flags ride on the first forward and the last backward step (grid transfers).
 		void sweep_pair_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, int first_flags = 0, int last_flags = 0 ) {
 			const uint64_t nc = L->num_colors;
-			const bool turnaround = L->ctx->fused_transfers && nc >= 2 && L->plan == nullptr
+			const bool turnaround = L->ctx->fused_transfers && nc >= 2
 				&& kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ nc - 1 ] ) );
 			for( uint64_t k = 0; k < nc; ++k ) {
 				const int flags = ( k == 0 ? first_flags : 0 ) | ( turnaround && k + 1 == nc ? 4 : 0 );
@@ -423,6 +425,23 @@ namespace slabgpu {
 		halo_exchange( L, z, -1 ); // z is the caller's: its ghost copies may be stale
 		color_step_enqueue( L, k, z, r );
 		L->stats.nnz_visited += L->color_nnz[ k ]; // smoother.hpp:71
+	}
+
+	// the same step applied twice in a row by one launch (the turnaround of a symmetric sweep); falls back to two
+	// steps where the kernel shape cannot repeat
+	void rbgs_color_step_twice( slab_level_s * L, uint64_t k, slab_vec_s * z, slab_vec_s * r ) {
+		check_smoother_args( L, z, r );
+		if( k >= L->num_colors ) {
+			fail( SLAB_ERR_INVALID_ARGUMENT, "rbgs_color_step_twice: colour index out of range" );
+		}
+		halo_exchange( L, z, -1 );
+		if( kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ k ] ) ) ) {
+			color_step_enqueue( L, k, z, r, 4 );
+		} else {
+			color_step_enqueue( L, k, z, r );
+			color_step_enqueue( L, k, z, r );
+		}
+		L->stats.nnz_visited += 2 * L->color_nnz[ k ];
 	}
 
 	void rbgs_forward( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) {

@@ -300,3 +300,30 @@ def test_full_size_eight_rank_vcycle_equals_global_bitwise(slab, ctx, kernel_fam
     if kernel_family != "default-kernels":
         pytest.skip("one pass at this size is enough: the default thresholds already select the coded kernels")
     _vcycle_case(slab, ctx, (2, 2, 2), (104, 104, 104), 4)
+
+
+@pytest.mark.parametrize("grid,local", [((2, 1, 1), (8, 8, 8)), ((2, 2, 2), (12, 12, 12)), ((1, 3, 2), (6, 4, 8)),
+                                         ((2, 1, 1), (104, 104, 104))])
+def test_sweep_turnaround_on_decomposed_levels(slab, ctx, grid, local):
+    """What the library's own symmetric sweep does on a decomposed level: colours 0..6 forward, colour 7 twice in
+    ONE launch with a single halo message after the second update, colours 6..0 backward. Must equal the global
+    forward-then-backward sweep bit for bit (the rows of a colour never read that colour's ghost copies, so the
+    intermediate values need not travel)."""
+    w = World(slab, grid, local, 1)
+    lv = w.levels(0)
+    n_global = int(np.prod(w.global_dims))
+    single = ctx.build_hierarchy(w.global_dims, 1)
+    zg, _ = ctx.random_vector(n_global, 41)
+    rg, _ = ctx.random_vector(n_global, 42)
+    z = w.scatter(lv, zg.values())
+    r = w.scatter(lv, rg.values())
+    slab.rbgs_forward(single, zg, rg)
+    slab.rbgs_backward(single, zg, rg)
+    for k in range(7):
+        w.color_step(lv, k, z, r)
+    for lvl, zz, rr in zip(lv, z, r):
+        slab.rbgs_color_step_twice(lvl, 7, zz, rr)
+    w.exchange(lv, z, 7)
+    for k in range(6, -1, -1):
+        w.color_step(lv, k, z, r)
+    assert np.array_equal(w.gather(lv, z), zg.values())
