@@ -489,6 +489,10 @@ namespace slab_b200 {
 		inline void rbgs_color_step( ProblemLevel & level, std::size_t k, DenseVector & z, const DenseVector & r ) {
 			check( slab_rbgs_color_step( level.handle(), k, z.handle(), r.handle() ) );
 		}
+		// extension: the step twice in a row as one launch (the turnaround of rbgs_symmetric)
+		inline void rbgs_color_step_twice( ProblemLevel & level, std::size_t k, DenseVector & z, const DenseVector & r ) {
+			check( slab_rbgs_color_step_twice( level.handle(), k, z.handle(), r.handle() ) );
+		}
 	} // namespace detail
 
 	// ---- multigrid.hpp
