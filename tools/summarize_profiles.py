@@ -42,7 +42,8 @@ def launch_list(name, workload):
     by_kernel = collections.defaultdict(float)
     for (kernel, _grid), v in agg.items():
         by_kernel[kernel] += v[1]
-    out = [f"# ncu launch list — {workload} ({len(rows)} launches captured, ≈3 CG iterations)",
+    iterations = sum(1 for kernel, _g, _us in rows if kernel.startswith("k_cg_record"))
+    out = [f"# ncu launch list — {workload} ({len(rows)} launches captured from the steady state of a solve, {iterations} CG iterations)",
            "", "`ncu --metrics gpu__time_duration.sum --clock-control none` on `bench.py`; per-launch times are cold-cache and",
            "serialised (ncu flushes caches and drops the programmatic overlap), so read the SHARES, not the absolutes.", "",
            "| kernel | grid | launches | total µs | avg µs | share |", "|---|---|---|---|---|---|"]
