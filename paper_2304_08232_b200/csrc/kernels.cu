@@ -158,25 +158,47 @@ namespace slabgpu {
 
 			// ------------------------------------------------------------ vector ops
 
-			__global__ void k_fill( double * __restrict__ v, uint64_t n, double value ) {
+			// 16-byte stores in a grid-stride loop: one 8-byte store per thread reaches only 1.9 TB/s on B200
+			// (tools/vector_ops_probe.py). `head` leading elements (0 or 1) bring the rest to a 16-byte boundary.
+			__global__ void __launch_bounds__( kBlock ) k_fill( double * __restrict__ v, uint64_t n, double value, uint64_t head ) {
 				dep_trigger();
 				dep_wait();
-				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( i < n ) {
-					v[ i ] = value;
+				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				if( tid < head ) {
+					v[ tid ] = value;
+				}
+				double2 * v2 = reinterpret_cast< double2 * >( v + head );
+				const uint64_t pairs = ( n - head ) >> 1;
+				const double2 both = make_double2( value, value );
+				for( uint64_t i = tid; i < pairs; i += stride ) {
+					v2[ i ] = both;
+				}
+				if( tid == 0 && ( ( n - head ) & 1 ) ) {
+					v[ n - 1 ] = value;
 				}
 			}
 
-			// operations.hpp:103 — w may alias x or y: each thread reads its inputs before writing
-			__global__ void k_waxpby( double * w, double alpha, const double * x, double beta, const double * y,
-				uint64_t n ) {
+			// operations.hpp:103 — w may alias x or y: each thread reads its inputs before writing.
+			// Two elements per thread and iteration through 16-byte accesses (all vectors start on 256-byte
+			// boundaries); the arithmetic per element is unchanged.
+			__global__ void __launch_bounds__( kBlock ) k_waxpby( double * w, double alpha, const double * x, double beta,
+				const double * y, uint64_t n ) {
 				dep_trigger();
 				dep_wait();
-				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( i < n ) {
-					const double ax = __dmul_rn( alpha, x[ i ] );
-					const double by = __dmul_rn( beta, y[ i ] );
-					w[ i ] = __dadd_rn( ax, by );
+				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				const uint64_t pairs = n >> 1;
+				for( uint64_t i = tid; i < pairs; i += stride ) {
+					const double2 xv = reinterpret_cast< const double2 * >( x )[ i ];
+					const double2 yv = reinterpret_cast< const double2 * >( y )[ i ];
+					double2 out;
+					out.x = __dadd_rn( __dmul_rn( alpha, xv.x ), __dmul_rn( beta, yv.x ) );
+					out.y = __dadd_rn( __dmul_rn( alpha, xv.y ), __dmul_rn( beta, yv.y ) );
+					reinterpret_cast< double2 * >( w )[ i ] = out;
+				}
+				if( tid == 0 && ( n & 1 ) ) {
+					w[ n - 1 ] = __dadd_rn( __dmul_rn( alpha, x[ n - 1 ] ), __dmul_rn( beta, y[ n - 1 ] ) );
 				}
 			}
 
@@ -270,21 +292,28 @@ namespace slabgpu {
 				__shared__ bool is_last;
 				dep_trigger();
 				dep_wait();
+				// 16-byte loads, two pairs in flight per thread and iteration; four independent chains
 				double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
 				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				const uint64_t pairs = n >> 1;
+				const double2 * x2 = reinterpret_cast< const double2 * >( x );
+				const double2 * y2 = reinterpret_cast< const double2 * >( y );
 				uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				for( ; i + 3 * stride < n; i += 4 * stride ) { // four independent loads in flight per thread
-					const double a0 = x[ i ], b0 = y[ i ];
-					const double a1 = x[ i + stride ], b1 = y[ i + stride ];
-					const double a2 = x[ i + 2 * stride ], b2 = y[ i + 2 * stride ];
-					const double a3 = x[ i + 3 * stride ], b3 = y[ i + 3 * stride ];
-					acc0 = __dadd_rn( acc0, __dmul_rn( a0, b0 ) );
-					acc1 = __dadd_rn( acc1, __dmul_rn( a1, b1 ) );
-					acc2 = __dadd_rn( acc2, __dmul_rn( a2, b2 ) );
-					acc3 = __dadd_rn( acc3, __dmul_rn( a3, b3 ) );
+				for( ; i + stride < pairs; i += 2 * stride ) {
+					const double2 a0 = x2[ i ], b0 = y2[ i ];
+					const double2 a1 = x2[ i + stride ], b1 = y2[ i + stride ];
+					acc0 = __dadd_rn( acc0, __dmul_rn( a0.x, b0.x ) );
+					acc1 = __dadd_rn( acc1, __dmul_rn( a0.y, b0.y ) );
+					acc2 = __dadd_rn( acc2, __dmul_rn( a1.x, b1.x ) );
+					acc3 = __dadd_rn( acc3, __dmul_rn( a1.y, b1.y ) );
 				}
-				for( ; i < n; i += stride ) {
-					acc0 = __dadd_rn( acc0, __dmul_rn( x[ i ], y[ i ] ) );
+				for( ; i < pairs; i += stride ) {
+					const double2 a0 = x2[ i ], b0 = y2[ i ];
+					acc0 = __dadd_rn( acc0, __dmul_rn( a0.x, b0.x ) );
+					acc1 = __dadd_rn( acc1, __dmul_rn( a0.y, b0.y ) );
+				}
+				if( blockIdx.x == 0 && threadIdx.x == 0 && ( n & 1 ) ) {
+					acc2 = __dadd_rn( acc2, __dmul_rn( x[ n - 1 ], y[ n - 1 ] ) );
 				}
 				const double acc = __dadd_rn( __dadd_rn( acc0, acc1 ), __dadd_rn( acc2, acc3 ) );
 				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, out, smem, &is_last );
@@ -768,20 +797,27 @@ namespace slabgpu {
 
 			// ------------------------------------------------------------ CG updates
 
-			__global__ void k_cg_update_p( double * p, const double * __restrict__ z, const double * __restrict__ scalars,
-				const unsigned int * __restrict__ iter_counter, uint64_t n ) {
+			__global__ void __launch_bounds__( kBlock ) k_cg_update_p( double * p, const double * __restrict__ z,
+				const double * __restrict__ scalars, const unsigned int * __restrict__ iter_counter, uint64_t n ) {
 				dep_trigger();
 				dep_wait();
-				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( i >= n ) {
-					return;
+				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				const uint64_t pairs = n >> 1;
+				const bool first = *iter_counter == 0u;
+				// cg.hpp:118  waxpby( p, 1.0, z, 0.0, z )  /  cg.hpp:120  waxpby( p, 1.0, z, rho / rho_prev, p )
+				const double beta = first ? 0.0 : __ddiv_rn( scalars[ S_RHO ], scalars[ S_RHO_PREV ] );
+				for( uint64_t i = tid; i < pairs; i += stride ) {
+					const double2 zv = reinterpret_cast< const double2 * >( z )[ i ];
+					const double2 pv = first ? zv : reinterpret_cast< const double2 * >( p )[ i ];
+					double2 out;
+					out.x = __dadd_rn( __dmul_rn( 1.0, zv.x ), __dmul_rn( beta, pv.x ) );
+					out.y = __dadd_rn( __dmul_rn( 1.0, zv.y ), __dmul_rn( beta, pv.y ) );
+					reinterpret_cast< double2 * >( p )[ i ] = out;
 				}
-				const double zi = z[ i ];
-				if( *iter_counter == 0u ) { // cg.hpp:118  waxpby( p, 1.0, z, 0.0, z )
-					p[ i ] = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 0.0, zi ) );
-				} else {                    // cg.hpp:120  waxpby( p, 1.0, z, rho / rho_prev, p )
-					const double beta = __ddiv_rn( scalars[ S_RHO ], scalars[ S_RHO_PREV ] );
-					p[ i ] = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( beta, p[ i ] ) );
+				if( tid == 0 && ( n & 1 ) ) {
+					const double zi = z[ n - 1 ];
+					p[ n - 1 ] = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( beta, first ? zi : p[ n - 1 ] ) );
 				}
 			}
 
@@ -812,12 +848,31 @@ namespace slabgpu {
 				const double alpha = __ddiv_rn( rho, scalars[ S_PQ ] );
 				double acc = 0.0;
 				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
-				for( uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x; i < n; i += stride ) {
+				const uint64_t pairs = n >> 1;
+				double acc1 = 0.0;
+				for( uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x; i < pairs; i += stride ) {
+					const double2 xv = reinterpret_cast< const double2 * >( x )[ i ];
+					const double2 pv = reinterpret_cast< const double2 * >( p )[ i ];
+					const double2 rv = reinterpret_cast< const double2 * >( r )[ i ];
+					const double2 qv = reinterpret_cast< const double2 * >( q )[ i ];
+					double2 xn, rn;
+					xn.x = __dadd_rn( __dmul_rn( 1.0, xv.x ), __dmul_rn( alpha, pv.x ) );
+					xn.y = __dadd_rn( __dmul_rn( 1.0, xv.y ), __dmul_rn( alpha, pv.y ) );
+					rn.x = __dadd_rn( __dmul_rn( 1.0, rv.x ), __dmul_rn( -alpha, qv.x ) );
+					rn.y = __dadd_rn( __dmul_rn( 1.0, rv.y ), __dmul_rn( -alpha, qv.y ) );
+					reinterpret_cast< double2 * >( x )[ i ] = xn;
+					reinterpret_cast< double2 * >( r )[ i ] = rn;
+					acc = __dadd_rn( acc, __dmul_rn( rn.x, rn.x ) );
+					acc1 = __dadd_rn( acc1, __dmul_rn( rn.y, rn.y ) );
+				}
+				if( blockIdx.x == 0 && threadIdx.x == 0 && ( n & 1 ) ) {
+					const uint64_t i = n - 1;
 					x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );
 					const double rn = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -alpha, q[ i ] ) );
 					r[ i ] = rn;
-					acc = __dadd_rn( acc, __dmul_rn( rn, rn ) );
+					acc1 = __dadd_rn( acc1, __dmul_rn( rn, rn ) );
 				}
+				acc = __dadd_rn( acc, acc1 );
 				if( blockIdx.x == 0 && threadIdx.x == 0 ) {
 					scalars[ S_RHO_PREV ] = rho;
 				}
@@ -893,11 +948,28 @@ namespace slabgpu {
 
 		// ================================================================ wrappers
 
+		namespace {
+			// grid of the vector kernels that move two elements per thread and iteration: one pass for short
+			// vectors, a grid-stride loop of about four iterations per thread for long ones
+			unsigned int vector_grid( uint64_t n ) {
+				const uint64_t pairs = ( n + 1 ) >> 1;
+				const uint64_t want = ( pairs + kBlock * 4 - 1 ) / ( kBlock * 4 );
+				const uint64_t floor_blocks = ( pairs + kBlock - 1 ) / kBlock;
+				const uint64_t small = floor_blocks < 148 * 4 ? floor_blocks : 148 * 4;
+				const uint64_t grid = want > small ? want : small;
+				return static_cast< unsigned int >( grid < 1 ? 1 : grid );
+			}
+		} // namespace
+
 		void fill( cudaStream_t st, double * v, uint64_t n, double value ) {
 			if( n == 0 ) {
 				return;
 			}
-			launch( k_fill, blocks_for( n ), kBlock, st, v, n, value );
+			const uint64_t head = ( reinterpret_cast< uintptr_t >( v ) & 15u ) != 0 && n > 0 ? 1 : 0;
+			const uint64_t pairs = ( n - head ) >> 1;
+			const uint64_t want = ( pairs + kBlock * 4 - 1 ) / ( kBlock * 4 ); // four stores per thread
+			const unsigned int grid = static_cast< unsigned int >( want < 1 ? 1 : ( want > 148 * 16 ? 148 * 16 : want ) );
+			launch( k_fill, grid, kBlock, st, v, n, value, head );
 		}
 
 		void waxpby( cudaStream_t st, double * w, double alpha, const double * x, double beta, const double * y,
@@ -905,7 +977,7 @@ namespace slabgpu {
 			if( n == 0 ) {
 				return;
 			}
-			launch( k_waxpby, blocks_for( n ), kBlock, st, w, alpha, x, beta, y, n );
+			launch( k_waxpby, vector_grid( n ), kBlock, st, w, alpha, x, beta, y, n );
 		}
 
 		void dot_exact( cudaStream_t st, const double * x, const double * y, uint64_t n, double * partials,
@@ -1129,7 +1201,7 @@ namespace slabgpu {
 			if( n == 0 ) {
 				return;
 			}
-			launch( k_cg_update_p, blocks_for( n ), kBlock, st, p, z, scalars, iter_counter, n );
+			launch( k_cg_update_p, vector_grid( n ), kBlock, st, p, z, scalars, iter_counter, n );
 		}
 
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
