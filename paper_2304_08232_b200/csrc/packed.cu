@@ -256,9 +256,12 @@ namespace slabgpu {
 			// one constant-cache access — unlike a shared-memory table, it takes nothing from the L1 data
 			// pipe, which the gathers saturate (measured: shared-memory lookups were 45% of its wavefronts).
 			template< int DICT >
-			struct DictParam {
-				double val[ DICT ];
-				int32_t delta[ DICT ];
+			struct DictParam { // value and offset of a code side by side: one index computation serves both reads
+				struct Entry {
+					double val;
+					int32_t delta;
+					int32_t unused;
+				} e[ DICT ];
 			};
 
 			// ordered row sum over the coded entries: acc = acc + val*xrow[delta] (xrow = x + row), ascending
@@ -280,7 +283,7 @@ namespace slabgpu {
 						for( int j = 0; j < 4; ++j ) {
 							if( 4 * ( w0 + b ) + j < NCODES ) {
 								const unsigned int code = ( rc.word( w0 + b ) >> ( 8 * j ) ) & 0xffu;
-								xv[ 4 * b + j ] = xrow[ dp.delta[ code ] ];
+								xv[ 4 * b + j ] = xrow[ dp.e[ code ].delta ];
 							}
 						}
 					}
@@ -288,7 +291,7 @@ namespace slabgpu {
 					// basic blocks, so a never-taken branch pins them (an empty asm only pins the front end)
 					if( BATCH > 1 ) {
 						asm volatile( "" ::: "memory" );
-						if( dp.delta[ 0 ] == 0x7fffffff ) { // entry 0 is {0.0, 0}
+						if( dp.e[ 0 ].delta == 0x7fffffff ) { // entry 0 is {0.0, 0}
 							__trap();
 						}
 					}
@@ -298,7 +301,7 @@ namespace slabgpu {
 						for( int j = 0; j < 4; ++j ) {
 							if( 4 * ( w0 + b ) + j < NCODES ) {
 								const unsigned int code = ( rc.word( w0 + b ) >> ( 8 * j ) ) & 0xffu;
-								const double sum = __dadd_rn( acc, __dmul_rn( dp.val[ code ], xv[ 4 * b + j ] ) );
+								const double sum = __dadd_rn( acc, __dmul_rn( dp.e[ code ].val, xv[ 4 * b + j ] ) );
 								if( RAGGED ) {
 									acc = code != 0u ? sum : acc;
 								} else {
@@ -348,7 +351,7 @@ namespace slabgpu {
 					return plain_row_sum< WANT_DIAG >( plain.slice_off, plain.vals, plain.cols, pos, x, row, diag );
 				}
 				if( WANT_DIAG ) {
-					diag = dp.val[ rc.diag_code() ];
+					diag = dp.e[ rc.diag_code() ].val;
 				}
 				if( warp_ragged ) {
 					return coded_row_sum< NCODES, CHUNKS, BATCH, true >( rc, x + row, dp );
@@ -504,8 +507,8 @@ namespace slabgpu {
 					for( int j = 0; j < 4; ++j ) {
 						if( 4 * wi + j < NCODES ) {
 							const unsigned int code = ( word >> ( 8 * j ) ) & 0xffu;
-							dl[ j ] = dp.delta[ code ];
-							v[ j ] = dp.val[ code ];
+							dl[ j ] = dp.e[ code ].delta;
+							v[ j ] = dp.e[ code ].val;
 						}
 					}
 					#pragma unroll
@@ -592,7 +595,7 @@ namespace slabgpu {
 							z[ i[ q ] ] = zi[ q ];
 						}
 					}
-					const double d = dp.val[ rc[ 0 ].diag_code() ];
+					const double d = dp.e[ rc[ 0 ].diag_code() ].val;
 					const int passes = ( flags & 4 ) ? 2 : 1; // see k_gs_color_packed
 					#pragma unroll 1
 					for( int pass = 0; pass < passes; ++pass ) {
@@ -728,7 +731,7 @@ namespace slabgpu {
 							z[ i[ q ] ] = zi[ q ];
 						}
 					}
-					const double d = dp.val[ lc.diag_code() ];
+					const double d = dp.e[ lc.diag_code() ].val;
 					const int passes = ( flags & 4 ) ? 2 : 1; // see k_gs_color_packed
 					#pragma unroll 1
 					for( int pass = 0; pass < passes; ++pass ) {
@@ -954,8 +957,8 @@ namespace slabgpu {
 			DictParam< DICT > dict_param( const Packed & P ) {
 				DictParam< DICT > dp;
 				for( int t = 0; t < DICT; ++t ) {
-					dp.val[ t ] = t < P.dict_size ? P.h_dict[ t ].val : 0.0;
-					dp.delta[ t ] = t < P.dict_size ? P.h_dict[ t ].delta : 0;
+					dp.e[ t ].val = t < P.dict_size ? P.h_dict[ t ].val : 0.0;
+					dp.e[ t ].delta = t < P.dict_size ? P.h_dict[ t ].delta : 0;
 				}
 				return dp;
 			}
