@@ -301,11 +301,9 @@ namespace slabgpu {
 						for( int j = 0; j < 4; ++j ) {
 							if( 4 * ( w0 + b ) + j < NCODES ) {
 								const unsigned int code = ( rc.word( w0 + b ) >> ( 8 * j ) ) & 0xffu;
-								const double sum = __dadd_rn( acc, __dmul_rn( dp.e[ code ].val, xv[ 4 * b + j ] ) );
-								if( RAGGED ) {
-									acc = code != 0u ? sum : acc;
-								} else {
-									acc = sum;
+								const double prod = __dmul_rn( dp.e[ code ].val, xv[ 4 * b + j ] );
+								if( !RAGGED || code != 0u ) { // a predicated add, not a select: padding adds nothing
+									acc = __dadd_rn( acc, prod );
 								}
 							}
 						}
@@ -525,11 +523,9 @@ namespace slabgpu {
 						#pragma unroll
 						for( int j = 0; j < 4; ++j ) {
 							if( 4 * wi + j < NCODES ) {
-								const double sum = __dadd_rn( acc[ r ], __dmul_rn( v[ j ], xv[ r ][ j ] ) );
-								if( RAGGED ) {
-									acc[ r ] = ( ( word >> ( 8 * j ) ) & 0xffu ) != 0u ? sum : acc[ r ];
-								} else {
-									acc[ r ] = sum;
+								const double prod = __dmul_rn( v[ j ], xv[ r ][ j ] );
+								if( !RAGGED || ( ( word >> ( 8 * j ) ) & 0xffu ) != 0u ) {
+									acc[ r ] = __dadd_rn( acc[ r ], prod );
 								}
 							}
 						}
