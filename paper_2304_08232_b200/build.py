@@ -32,9 +32,31 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA extension cannot be built")
 
 
+STAMP = LIB + ".stamp"
+
+
+def _source_digest() -> str:
+    """sha256 over the sources, headers and flags the library is built from. The stamp next to the .so
+    records it, so a copied tree (gpurun snapshot, fresh checkout + shipped .so) is recognised as up to
+    date whatever the copy did to the file times."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.normpath(os.path.join(CSRC, x)) for x in HEADERS]
+    for d in deps:
+        if os.path.exists(d):
+            h.update(d[len(HERE):].encode())
+            with open(d, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
+    if os.path.exists(STAMP):
+        with open(STAMP) as fh:
+            return fh.read().strip() != _source_digest()
     built = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     deps += [os.path.normpath(os.path.join(CSRC, h)) for h in HEADERS]
@@ -87,6 +109,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed linking libslab_b200.so")
     with open(os.path.join(HERE, "build_ptxas.log"), "w") as fh:
         fh.write("\n".join(r[2] for r in results))
+    with open(STAMP, "w") as fh:
+        fh.write(_source_digest() + "\n")
     return LIB
 
 
