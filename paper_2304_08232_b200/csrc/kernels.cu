@@ -14,6 +14,10 @@
 //    and preload their matrix rows while the previous kernel drains; `griddepcontrol.wait` then
 //    orders every access to mutable data (vectors, scalars) after the previous kernel's writes.
 //    EVERY kernel executes the wait before touching mutable memory, so ordering is transitive.
+//    Pointers to data an earlier kernel of the stream may have written (vectors, scalars, partials) are
+//    never `const __restrict__`: such loads become read-only-path loads that the compiler may hoist above
+//    the wait (it did, once, in the exact dot: right results without PDL, wrong ones with it). Only the
+//    immutable matrix data (values, columns, codes, row lists, masks) is __restrict__.
 //  * Vector gathers (x / z) are served by L1/L2.
 #include "kernels.cuh"
 
@@ -160,7 +164,7 @@ namespace slabgpu {
 
 			// 16-byte stores in a grid-stride loop: one 8-byte store per thread reaches only 1.9 TB/s on B200
 			// (tools/vector_ops_probe.py). `head` leading elements (0 or 1) bring the rest to a 16-byte boundary.
-			__global__ void __launch_bounds__( kBlock ) k_fill( double * __restrict__ v, uint64_t n, double value, uint64_t head ) {
+			__global__ void __launch_bounds__( kBlock ) k_fill( double * v, uint64_t n, double value, uint64_t head ) {
 				dep_trigger();
 				dep_wait();
 				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -202,36 +206,71 @@ namespace slabgpu {
 				}
 			}
 
-			// operations.hpp:61-91: one warp per 4096-element chunk. The 32 lanes form the rounded
-			// products in parallel (coalesced), lane 0 then adds them left to right; the block that
-			// finishes last adds the per-chunk partials in chunk order.
-			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * __restrict__ x,
-				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
-				__shared__ double prod[ kDotChunk ];
+			// operations.hpp:61-91: one warp per 4096-element chunk. The chunk's rounded products are added left
+			// to right by lane 0 — a chain of 4096 dependent additions (8.8 cycles each on B200,
+			// tools/probes/fp64_latency.cu), which is what this kernel costs. Everything else hides behind it:
+			// the chunk moves through shared memory in tiles of 512 products, and while lane 0 adds one tile all
+			// 32 lanes already hold the loads of the next tile in flight. 8 KB of shared memory per warp keeps
+			// every chunk of a 192^3 vector resident at once. The block that finishes last adds the per-chunk
+			// partials in chunk order.
+			constexpr int kDotTile = 512;
+			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * x,
+				const double * y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
+				__shared__ double prod[ 2 ][ kDotTile ];
 				dep_trigger();
 				dep_wait();
 				const uint64_t begin = static_cast< uint64_t >( blockIdx.x ) * kDotChunk;
 				const uint64_t remaining = n - begin;
 				const int len = static_cast< int >( remaining < kDotChunk ? remaining : kDotChunk );
 				const int lane = threadIdx.x;
-				for( int i = lane; i < len; i += 32 ) {
-					prod[ i ] = __dmul_rn( x[ begin + i ], y[ begin + i ] );
-				}
-				__syncwarp();
-				if( lane == 0 ) {
-					double acc = 0.0;
-					#pragma unroll 16
-					for( int i = 0; i < len; ++i ) {
-						acc = __dadd_rn( acc, prod[ i ] );
+				const int ntiles = ( len + kDotTile - 1 ) / kDotTile;
+				constexpr int kPer = kDotTile / 32; // products per lane and tile
+				double a[ kPer ], c[ kPer ];
+				const auto tile_load = [ & ]( int t ) { // coalesced: lane l takes elements l, l + 32, ... of the tile
+					#pragma unroll
+					for( int k = 0; k < kPer; ++k ) {
+						const int i = t * kDotTile + k * 32 + lane;
+						a[ k ] = i < len ? x[ begin + i ] : 0.0;
+						c[ k ] = i < len ? y[ begin + i ] : 0.0;
 					}
+				};
+				const auto tile_store = [ & ]( int t ) {
+					#pragma unroll
+					for( int k = 0; k < kPer; ++k ) {
+						prod[ t & 1 ][ k * 32 + lane ] = __dmul_rn( a[ k ], c[ k ] );
+					}
+				};
+				tile_load( 0 );
+				tile_store( 0 );
+				__syncwarp();
+				double acc = 0.0;
+				for( int t = 0; t < ntiles; ++t ) {
+					if( t + 1 < ntiles ) {
+						tile_load( t + 1 ); // in flight while the chain below runs
+					}
+					const int count = len - t * kDotTile < kDotTile ? len - t * kDotTile : kDotTile;
+					if( lane == 0 ) {
+						const double * p = prod[ t & 1 ];
+						#pragma unroll 16
+						for( int i = 0; i < count; ++i ) {
+							acc = __dadd_rn( acc, p[ i ] );
+						}
+					}
+					if( t + 1 < ntiles ) {
+						tile_store( t + 1 );
+					}
+					__syncwarp();
+				}
+				if( lane == 0 ) {
 					partials[ blockIdx.x ] = acc;
 					__threadfence();
 					const unsigned int ticket = atomicAdd( counter, 1u );
 					if( ticket == gridDim.x - 1 ) {
 						__threadfence();
 						double total = 0.0;
-						for( unsigned int c = 0; c < gridDim.x; ++c ) {
-							total = __dadd_rn( total, __ldcg( partials + c ) );
+						#pragma unroll 8
+						for( unsigned int k = 0; k < gridDim.x; ++k ) {
+							total = __dadd_rn( total, __ldcg( partials + k ) );
 						}
 						*out = total;
 						*counter = 0u;
@@ -271,7 +310,7 @@ namespace slabgpu {
 			}
 
 			// one block folds `count` block partials in a fixed order (each thread a strided chain, then the tree)
-			__global__ void __launch_bounds__( 1024 ) k_sum_partials( const double * __restrict__ partials, uint64_t count,
+			__global__ void __launch_bounds__( 1024 ) k_sum_partials( const double * partials, uint64_t count,
 				double * out ) {
 				__shared__ double smem[ 32 ];
 				dep_trigger();
@@ -286,8 +325,8 @@ namespace slabgpu {
 				}
 			}
 
-			__global__ void __launch_bounds__( kBlock ) k_dot_tree( const double * __restrict__ x,
-				const double * __restrict__ y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
+			__global__ void __launch_bounds__( kBlock ) k_dot_tree( const double * x,
+				const double * y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
 				__shared__ double smem[ 32 ];
 				__shared__ bool is_last;
 				dep_trigger();
@@ -324,8 +363,8 @@ namespace slabgpu {
 			// operations.hpp:164-174. MASKED: one thread per mask member, others untouched.
 			template< bool MASKED >
 			__global__ void __launch_bounds__( kBlock ) k_spmv( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, const int32_t * __restrict__ members, int64_t count, double * dot_partials,
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * x,
+				double * y, const int32_t * __restrict__ members, int64_t count, double * dot_partials,
 				unsigned int * dot_counter, double * dot_out ) {
 				__shared__ double smem[ 32 ];
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -372,8 +411,8 @@ namespace slabgpu {
 			//    zero[k] = 0 prepares the coarse guess (multigrid.hpp:104).
 			__global__ void __launch_bounds__( kBlock, 2 ) k_gs_color( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
-				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
+				const double * src, double * out, double * zero,
 				const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
 				// pos_list: the launch covers exactly these positions (the boundary rows of a colour, computed
 				// first so that their halo messages travel while the interior rows run); skip: positions
@@ -432,8 +471,8 @@ namespace slabgpu {
 			// member is the fine point of coarse index p): f = 1*r + (-1)*(A z), r_c = 0 + 1*f.
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
-				double * __restrict__ r_c, double * __restrict__ zero ) {
+				int64_t n_coarse, const double * z, const double * r,
+				double * r_c, double * zero ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const bool live = p < n_coarse;
 				int32_t i = 0;
@@ -523,8 +562,8 @@ namespace slabgpu {
 			template< int B, int MINBLOCKS >
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_batched( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r,
-				const double * __restrict__ src, const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
+				int64_t pos_begin, int64_t pos_count, double * z, const double * r,
+				const double * src, const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -553,8 +592,8 @@ namespace slabgpu {
 
 			template< int B, int MINBLOCKS >
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_spmv_batched( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * __restrict__ x,
-				double * __restrict__ y, int64_t nrows, double * dot_partials, unsigned int * dot_counter, double * dot_out ) {
+				const double * __restrict__ vals, const int32_t * __restrict__ cols, const double * x,
+				double * y, int64_t nrows, double * dot_partials, unsigned int * dot_counter, double * dot_out ) {
 				__shared__ double smem[ 32 ];
 				dep_trigger();
 				dep_wait();
@@ -762,8 +801,8 @@ namespace slabgpu {
 
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_stream( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ cols, const int32_t * __restrict__ rows,
-				int64_t n_coarse, const double * __restrict__ z, const double * __restrict__ r,
-				double * __restrict__ r_c, double * __restrict__ zero ) {
+				int64_t n_coarse, const double * z, const double * r,
+				double * r_c, double * zero ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -783,7 +822,7 @@ namespace slabgpu {
 			// multigrid.hpp:71-81 at the injected rows: f[i] = 0 + 1*z_c[p]; z[i] = 1*z[i] + 1*f[i].
 			// (Elsewhere the reference computes z + 0.0, which only turns -0.0 into +0.0.)
 			__global__ void k_prolong_add( const int32_t * __restrict__ rows, int64_t n_coarse, double * z,
-				const double * __restrict__ z_c ) {
+				const double * z_c ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const int32_t i = p < n_coarse ? rows[ p ] : -1;
 				dep_trigger();
@@ -797,8 +836,8 @@ namespace slabgpu {
 
 			// ------------------------------------------------------------ CG updates
 
-			__global__ void __launch_bounds__( kBlock ) k_cg_update_p( double * p, const double * __restrict__ z,
-				const double * __restrict__ scalars, const unsigned int * __restrict__ iter_counter, uint64_t n ) {
+			__global__ void __launch_bounds__( kBlock ) k_cg_update_p( double * p, const double * z,
+				const double * scalars, const unsigned int * iter_counter, uint64_t n ) {
 				dep_trigger();
 				dep_wait();
 				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -821,8 +860,8 @@ namespace slabgpu {
 				}
 			}
 
-			__global__ void k_cg_update_xr( double * x, double * r, const double * __restrict__ p,
-				const double * __restrict__ q, double * scalars, uint64_t n ) {
+			__global__ void k_cg_update_xr( double * x, double * r, const double * p,
+				const double * q, double * scalars, uint64_t n ) {
 				dep_trigger();
 				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -838,8 +877,8 @@ namespace slabgpu {
 			}
 
 			// the same update with r'r (cg.hpp:132) reduced in the tree-dot shape on the way out
-			__global__ void __launch_bounds__( kBlock ) k_cg_update_xr_dot( double * x, double * r, const double * __restrict__ p,
-				const double * __restrict__ q, double * scalars, uint64_t n, double * partials, unsigned int * counter ) {
+			__global__ void __launch_bounds__( kBlock ) k_cg_update_xr_dot( double * x, double * r, const double * p,
+				const double * q, double * scalars, uint64_t n, double * partials, unsigned int * counter ) {
 				__shared__ double smem[ 32 ];
 				__shared__ bool is_last;
 				dep_trigger();
@@ -879,7 +918,7 @@ namespace slabgpu {
 				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, scalars + S_RR, smem, &is_last );
 			}
 
-			__global__ void k_cg_record( const double * __restrict__ scalars, double * hist_rr, double * hist_pq,
+			__global__ void k_cg_record( const double * scalars, double * hist_rr, double * hist_pq,
 				unsigned int * iter_counter ) {
 				dep_trigger();
 				dep_wait();
@@ -891,7 +930,7 @@ namespace slabgpu {
 
 			// ---- prototype: colour-major ("P") vector layout. Vector entry of row position p lives at p.
 			__global__ void k_permute_cols( const int32_t * __restrict__ cols, const int32_t * __restrict__ nat2pos,
-				int64_t entries, int32_t * __restrict__ out ) {
+				int64_t entries, int32_t * out ) {
 				const int64_t e = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( e < entries ) {
 					const int32_t c = cols[ e ];
@@ -905,7 +944,7 @@ namespace slabgpu {
 				}
 			}
 			__global__ void k_gather_to_pos( const int32_t * __restrict__ rows, int64_t npos, const double * __restrict__ nat,
-				double * __restrict__ pos ) {
+				double * pos ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				if( p < npos ) {
 					pos[ p ] = rows[ p ] >= 0 ? nat[ rows[ p ] ] : 0.0;
@@ -914,7 +953,7 @@ namespace slabgpu {
 			template< int B, int MINBLOCKS >
 			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_pos( const int64_t * __restrict__ slice_off,
 				const double * __restrict__ vals, const int32_t * __restrict__ pcols, int64_t pos_begin, int64_t pos_count,
-				double * z, const double * __restrict__ r ) {
+				double * z, const double * r ) {
 				dep_trigger();
 				dep_wait();
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;

@@ -397,8 +397,8 @@ namespace slabgpu {
 			template< int NCODES, int CHUNKS, int BATCH, int DICT >
 			__global__ void __launch_bounds__( kBlock, 4 ) k_gs_color_packed( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
-				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
+				const double * src, double * out, double * zero,
 				const int32_t * __restrict__ pos_list, const uint8_t * __restrict__ skip ) {
 				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				int32_t i = -1;
@@ -447,7 +447,7 @@ namespace slabgpu {
 			template< int NCODES, int CHUNKS, int BATCH, int DICT >
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_packed( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
-				int64_t n_coarse, const double * z, const double * __restrict__ r, double * r_c, double * zero ) {
+				int64_t n_coarse, const double * z, const double * r, double * r_c, double * zero ) {
 				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const bool live = p < n_coarse;
 				int32_t i = 0;
@@ -547,8 +547,8 @@ namespace slabgpu {
 			template< int NCODES, int CHUNKS, int R, int DICT >
 			__global__ void __launch_bounds__( kBlock, GS_MULTI_MINBLOCKS ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
-				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero ) {
+				int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
+				const double * src, double * out, double * zero ) {
 				const int lane = threadIdx.x & 31;
 				const unsigned int gw = ( blockIdx.x * blockDim.x + threadIdx.x ) >> 5;
 				const int64_t slice0 = multi_first_slice< R >( pos_begin >> 5, gw, static_cast< unsigned int >( stride ) );
@@ -658,8 +658,8 @@ namespace slabgpu {
 			template< int NCODES, int CHUNKS, int R, int DICT >
 			__global__ void __launch_bounds__( kBlock ) k_gs_color_packed_multi_skip( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
-				int64_t pos_begin, int64_t pos_count, double * z, const double * __restrict__ r, int flags,
-				const double * __restrict__ src, double * __restrict__ out, double * __restrict__ zero,
+				int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
+				const double * src, double * out, double * zero,
 				const uint8_t * __restrict__ skip ) {
 				// skip: positions flagged here are left out (the interior launch of a colour on a decomposed level,
 				// whose boundary rows went first); such rows — like the padding at the end of the range — take part in
