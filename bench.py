@@ -437,6 +437,17 @@ def main():
         line["roofline"] = roofline
 
     if not args.no_extras:
+        # the same solve from the plain SELL-32 arrays (12 B per stored entry, the format SURVEY's byte model
+        # describes): what the dictionary-coded copy buys, and the number to hold against the 12 B/nnz roofline
+        slab.set_tuning("packed", 0)
+        try:
+            time_solves(slab, ctx, h, b, main_run["x0"], cfg, 2, ctx.DenseVector(n))
+            plain_ms, _ = time_solves(slab, ctx, h, b, main_run["x0"], cfg, 3, ctx.DenseVector(n))
+        finally:
+            slab.set_tuning("packed", 1)
+        plain_per = plain_ms / 3
+        line["plain_sell_format"] = {"value": flops_step / (plain_per * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": plain_per,
+                                     "hbm_frac_of_measured_peak": iter_bytes * CG_ITERS / (plain_per * 1e-3) / 1e9 / peak}
         others = []
         for name in ("hpcg104", "hpcg64"):
             if name == args.workload:
