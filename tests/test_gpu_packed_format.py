@@ -265,3 +265,31 @@ def test_microbench_256_checksums_with_both_kernel_families(slab, ctx, tune):
                "dot_rz_after_symmetric": slab.dot(r, z)}
         for key, value in got.items():
             assert value == float.fromhex(gold[key + "_hex"]), (key, packed)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_banded_matrices_coded_equals_plain(slab, ctx, tune, seed):
+    """randomised shapes: row counts that are no multiple of 32, 2 to 60 bands at random offsets with random
+    values (so the width class, the dictionary size, the stride vote and the ragged ends all vary), a few rows
+    with private entries (escapes); every coded kernel shape must equal the plain kernels bit for bit"""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(40, 1500))
+    nbands = int(rng.integers(2, 61))
+    offsets = sorted(set(int(o) for o in rng.integers(-min(n - 1, 400), min(n - 1, 400) + 1, size=nbands) if o != 0))
+    values = [float(rng.integers(-8, 9)) / 4.0 or -0.25 for _ in offsets]
+    rows = banded(n, offsets, values, float(len(offsets)) * 3.0 + 1.0)
+    for i in rng.choice(n, size=int(rng.integers(0, max(1, n // 40))), replace=False):
+        rows[int(i)][int(rng.integers(0, n))] = float(rng.random()) + 0.125
+        rows[int(i)][int(i)] = float(len(offsets)) * 3.0 + 1.0
+    csr = csr_from_rows(rows, n)
+    lvl = slab.ProblemLevel(ctx, csr)
+    x, _ = ctx.random_vector(n, 5 + seed)
+    r, _ = ctx.random_vector(n, 6 + seed)
+    z0, _ = ctx.random_vector(n, 7 + seed)
+    tune(packed=0)
+    plain = run_level_ops(slab, ctx, lvl, x.values(), r.values(), z0.values())
+    for shape in SHAPES:
+        tune(packed=1, packed_min_rows=0, packed_multi_min_rows=0, **shape)
+        got = run_level_ops(slab, ctx, lvl, x.values(), r.values(), z0.values())
+        for key in plain:
+            assert np.array_equal(got[key], plain[key]), (key, shape, lvl.A.format_info(), lvl.format_info())
