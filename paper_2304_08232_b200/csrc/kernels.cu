@@ -220,34 +220,43 @@ namespace slabgpu {
 			// instead of the 8.8 of the addition alone).
 			__device__ __forceinline__ double chain_sum( const double * p, int count, double acc ) {
 				constexpr int kStep = 16;
-				double cur[ kStep ], nxt[ kStep ];
+				double ra[ kStep ], rb[ kStep ]; // two register sets that swap roles statically (no copies)
 				#pragma unroll
 				for( int k = 0; k < kStep; ++k ) {
-					cur[ k ] = k < count ? p[ k ] : 0.0;
+					ra[ k ] = k < count ? p[ k ] : 0.0;
 				}
 				int i = 0;
-				for( ; i + kStep <= count; i += kStep ) {
+				for( ; i + 2 * kStep <= count; i += 2 * kStep ) {
 					#pragma unroll
 					for( int k = 0; k < kStep; ++k ) {
-						nxt[ k ] = i + kStep + k < count ? p[ i + kStep + k ] : 0.0;
+						rb[ k ] = p[ i + kStep + k ];
 					}
 					#pragma unroll
 					for( int k = 0; k < kStep; ++k ) {
-						acc = __dadd_rn( acc, cur[ k ] );
+						acc = __dadd_rn( acc, ra[ k ] );
 					}
 					#pragma unroll
 					for( int k = 0; k < kStep; ++k ) {
-						cur[ k ] = nxt[ k ];
+						ra[ k ] = i + 2 * kStep + k < count ? p[ i + 2 * kStep + k ] : 0.0;
+					}
+					#pragma unroll
+					for( int k = 0; k < kStep; ++k ) {
+						acc = __dadd_rn( acc, rb[ k ] );
 					}
 				}
+				// fewer than 32 left: ra holds the next 16 (zero beyond count)
 				#pragma unroll
-				for( int k = 0; k < kStep; ++k ) { // the last, partial group
+				for( int k = 0; k < kStep; ++k ) {
 					if( i + k < count ) {
-						acc = __dadd_rn( acc, cur[ k ] );
+						acc = __dadd_rn( acc, ra[ k ] );
 					}
+				}
+				for( int j = i + kStep; j < count; ++j ) {
+					acc = __dadd_rn( acc, p[ j ] );
 				}
 				return acc;
 			}
+
 			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * x,
 				const double * y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
 				__shared__ double prod[ 2 ][ kDotTile ];
