@@ -489,8 +489,10 @@ namespace slabgpu {
 			}
 
 			template< int NCODES, int CHUNKS, int R, bool RAGGED, int DICT >
-			__device__ __forceinline__ void shared_rows_sum( const RowCodes< CHUNKS > & rc, const double * const ( &xrow )[ R ],
+			__device__ __forceinline__ void shared_rows_sum( const RowCodes< CHUNKS > & rc, const double * x, const int32_t ( &row )[ R ],
 				const DictParam< DICT > & dp, double ( &acc )[ R ] ) {
+				// (row + delta in 32 bits, then one widening multiply-add per gather: with per-row pointers the
+				//  compiler rebuilds each 64-bit address from the row index, five instructions per gather)
 				constexpr int WORDS = ( NCODES + 3 ) / 4;
 				#pragma unroll
 				for( int r = 0; r < R; ++r ) {
@@ -514,7 +516,7 @@ namespace slabgpu {
 						#pragma unroll
 						for( int j = 0; j < 4; ++j ) {
 							if( 4 * wi + j < NCODES ) {
-								xv[ r ][ j ] = xrow[ r ][ dl[ j ] ];
+								xv[ r ][ j ] = x[ row[ r ] + dl[ j ] ];
 							}
 						}
 					}
@@ -579,12 +581,10 @@ namespace slabgpu {
 				const bool warp_ragged = __any_sync( 0xffffffffu, rc[ 0 ].template ragged< NCODES >() );
 				if( shared ) {
 					double ri[ R ], zi[ R ], acc[ R ];
-					const double * zrow[ R ];
 					#pragma unroll
 					for( int q = 0; q < R; ++q ) {
 						ri[ q ] = r[ i[ q ] ];
 						zi[ q ] = z[ i[ q ] ];
-						zrow[ q ] = z + i[ q ];
 						if( flags & 1 ) {
 							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ pos[ q ] - pos_begin ] ) );
 							zi[ q ] = __dadd_rn( __dmul_rn( 1.0, zi[ q ] ), __dmul_rn( 1.0, f ) );
@@ -596,9 +596,9 @@ namespace slabgpu {
 					#pragma unroll 1
 					for( int pass = 0; pass < passes; ++pass ) {
 						if( warp_ragged ) {
-							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], z, i, dp, acc );
 						} else {
-							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], z, i, dp, acc );
 						}
 						#pragma unroll
 						for( int q = 0; q < R; ++q ) {
@@ -608,9 +608,9 @@ namespace slabgpu {
 					}
 					if( flags & 2 ) {
 						if( warp_ragged ) {
-							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], z, i, dp, acc );
 						} else {
-							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], z, i, dp, acc );
 						}
 						#pragma unroll
 						for( int q = 0; q < R; ++q ) {
@@ -714,13 +714,12 @@ namespace slabgpu {
 				const bool warp_ragged = __any_sync( 0xffffffffu, lc.template ragged< NCODES >() );
 				if( shared ) {
 					double ri[ R ], zi[ R ], acc[ R ];
-					const double * zrow[ R ];
+					int32_t at[ R ];
 					#pragma unroll
 					for( int q = 0; q < R; ++q ) {
-						const int32_t at = i[ q ] >= 0 ? i[ q ] : li; // passengers read the leader's row (row 0 on idle lanes)
-						ri[ q ] = r[ at ];
-						zi[ q ] = z[ at ];
-						zrow[ q ] = z + at;
+						at[ q ] = i[ q ] >= 0 ? i[ q ] : li; // passengers read the leader's row (row 0 on idle lanes)
+						ri[ q ] = r[ at[ q ] ];
+						zi[ q ] = z[ at[ q ] ];
 						if( ( flags & 1 ) && i[ q ] >= 0 ) {
 							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ pos[ q ] - pos_begin ] ) );
 							zi[ q ] = __dadd_rn( __dmul_rn( 1.0, zi[ q ] ), __dmul_rn( 1.0, f ) );
@@ -732,9 +731,9 @@ namespace slabgpu {
 					#pragma unroll 1
 					for( int pass = 0; pass < passes; ++pass ) {
 						if( warp_ragged ) {
-							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, z, at, dp, acc );
 						} else {
-							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, z, at, dp, acc );
 						}
 						#pragma unroll
 						for( int q = 0; q < R; ++q ) {
@@ -746,9 +745,9 @@ namespace slabgpu {
 					}
 					if( flags & 2 ) {
 						if( warp_ragged ) {
-							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, true >( lc, z, at, dp, acc );
 						} else {
-							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, zrow, dp, acc );
+							shared_rows_sum< NCODES, CHUNKS, R, false >( lc, z, at, dp, acc );
 						}
 						#pragma unroll
 						for( int q = 0; q < R; ++q ) {
@@ -830,15 +829,15 @@ namespace slabgpu {
 				double prod = 0.0;
 				if( shared ) {
 					double acc[ R ];
-					const double * xrow[ R ];
+					int32_t row32[ R ];
 					#pragma unroll
 					for( int q = 0; q < R; ++q ) {
-						xrow[ q ] = x + row[ q ];
+						row32[ q ] = static_cast< int32_t >( row[ q ] );
 					}
 					if( warp_ragged ) {
-						shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], xrow, dp, acc );
+						shared_rows_sum< NCODES, CHUNKS, R, true >( rc[ 0 ], x, row32, dp, acc );
 					} else {
-						shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], xrow, dp, acc );
+						shared_rows_sum< NCODES, CHUNKS, R, false >( rc[ 0 ], x, row32, dp, acc );
 					}
 					#pragma unroll
 					for( int q = 0; q < R; ++q ) {
