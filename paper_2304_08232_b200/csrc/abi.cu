@@ -101,6 +101,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_packed_rows_spmv = static_cast< int >( value );
 		} else if( k == "packed_multi_min_rows" ) {
 			g_packed_multi_min_rows = value;
+		} else if( k == "cluster_rows" ) {
+			g_cluster_rows = value;
 		} else if( k == "packed_batch" ) {
 			g_packed_batch = static_cast< int >( value );
 		} else if( k == "packed_min_rows" ) {
@@ -275,6 +277,9 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_PACKED" ) ) {
 			g_use_packed = std::atoi( v ) ? 1 : 0;
+		}
+		if( const char * v = std::getenv( "SLAB_CLUSTER_ROWS" ) ) {
+			g_cluster_rows = std::atoll( v );
 		}
 		if( const char * v = std::getenv( "SLAB_KEEP_PLAIN" ) ) {
 			g_keep_plain = std::atoi( v ) ? 1 : 0;

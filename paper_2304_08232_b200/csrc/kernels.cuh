@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include <vector>
+
 #include <cuda_runtime.h>
 
 namespace slabgpu {
@@ -47,6 +49,13 @@ namespace slabgpu {
 		// pos_list: cover exactly these positions (pos_count = their number); skip: leave flagged positions out
 		// window_bytes > 0: size of z; many-wave launches then ask the L2 to keep z in its persisting carve-out
 		bool gs_color_step_can_fuse_residual( const Sell & S, int64_t pos_count );
+		// sweep_cluster.cu: one forward + one backward sweep of a small level in ONE launch (a thread-block cluster that
+		// separates the colours with its hardware barrier); first_flags / last_flags as the flags of gs_color_step on
+		// the first and the last step. Usable when the level has a coded copy and no colour above g_cluster_rows rows.
+		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size );
+		void gs_sweep_cluster( cudaStream_t st, const Sell & S, const int32_t * rows, const std::vector< int64_t > & color_pos,
+			const std::vector< uint64_t > & color_size, double * z, const double * r, int first_flags, int last_flags,
+			const double * src, double * out, double * zero );
 
 		// ---- fused grid transfers (multigrid.hpp:100-104 and :71-81)
 		// r_c[p] = 0 + 1*( 1*r[i] + (-1)*(A z)[i] ),  i = rows[p], p in the colour-0 block = injected rows

@@ -399,6 +399,15 @@ namespace slabgpu {
 		// first_flags / last_flags ride on the first forward and the last backward step (grid transfers).
 		void sweep_pair_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, int first_flags = 0, int last_flags = 0 ) {
 			const uint64_t nc = L->num_colors;
+			// small level on one process: the whole pair of sweeps in one launch (sweep_cluster.cu), same steps
+			if( L->ctx->fused_transfers && L->plan == nullptr && nc >= 1
+				&& kern::gs_sweep_cluster_usable( L->colorA, L->color_pos, L->color_size ) ) {
+				const int flags = first_flags | last_flags;
+				kern::gs_sweep_cluster( L->ctx->stream, L->colorA, L->d_rows, L->color_pos, L->color_size, z->d, r->d,
+					first_flags, last_flags, ( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr,
+					( flags & 2 ) ? L->z_c->d : nullptr );
+				return;
+			}
 			const bool turnaround = L->ctx->fused_transfers && nc >= 2
 				&& kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ nc - 1 ] ) );
 			for( uint64_t k = 0; k < nc; ++k ) {
