@@ -52,9 +52,10 @@ namespace slabgpu {
 		// sweep_cluster.cu: one forward + one backward sweep of a small level in ONE launch (a thread-block cluster that
 		// separates the colours with its hardware barrier); first_flags / last_flags as the flags of gs_color_step on
 		// the first and the last step. Usable when the level has a coded copy and no colour above g_cluster_rows rows.
-		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size );
+		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size,
+			uint64_t n );
 		void gs_sweep_cluster( cudaStream_t st, const Sell & S, const int32_t * rows, const std::vector< int64_t > & color_pos,
-			const std::vector< uint64_t > & color_size, double * z, const double * r, int first_flags, int last_flags,
+			const std::vector< uint64_t > & color_size, uint64_t n, double * z, const double * r, int first_flags, int last_flags,
 			const double * src, double * out, double * zero );
 
 		// ---- fused grid transfers (multigrid.hpp:100-104 and :71-81)

@@ -401,9 +401,9 @@ namespace slabgpu {
 			const uint64_t nc = L->num_colors;
 			// small level on one process: the whole pair of sweeps in one launch (sweep_cluster.cu), same steps
 			if( L->ctx->fused_transfers && L->plan == nullptr && nc >= 1
-				&& kern::gs_sweep_cluster_usable( L->colorA, L->color_pos, L->color_size ) ) {
+				&& kern::gs_sweep_cluster_usable( L->colorA, L->color_pos, L->color_size, L->n ) ) {
 				const int flags = first_flags | last_flags;
-				kern::gs_sweep_cluster( L->ctx->stream, L->colorA, L->d_rows, L->color_pos, L->color_size, z->d, r->d,
+				kern::gs_sweep_cluster( L->ctx->stream, L->colorA, L->d_rows, L->color_pos, L->color_size, L->n, z->d, r->d,
 					first_flags, last_flags, ( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr,
 					( flags & 2 ) ? L->z_c->d : nullptr );
 				return;

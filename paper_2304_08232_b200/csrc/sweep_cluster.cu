@@ -3,22 +3,28 @@
 // Why. A colour step of a coarse level is a few hundred to a few thousand rows: its kernel runs at the floor
 // of a dependent launch (2.2 us on B200 inside a CUDA graph with programmatic launches), and a symmetric sweep
 // is fifteen of them (smoother.hpp:108-111). Here one thread-block cluster (up to 16 CTAs, one row per thread)
-// walks the colours of the sweep itself and separates them with the cluster's hardware barrier
-// (barrier.cluster, release/acquire at cluster scope) instead of a kernel boundary. Everything a row needs that
-// the sweep does not change — its codes, its row index, r[i] — sits in shared memory from the prologue on, so a
-// phase is barrier -> one round of gathers from the L2 -> the row's add chain -> store -> barrier.
+// walks the colours of the sweep itself and separates them with the cluster's hardware barrier instead of a
+// kernel boundary. Everything a row needs that the sweep does not change — its codes, its row index, r[i] — sits
+// in shared memory from the prologue on, and so does z: every CTA holds a full copy, gathers from its own copy
+// and stores a row's new value into every copy through distributed shared memory. A phase is then
+// barrier -> shared-memory gathers -> the row's add chain and divide -> 16 stores -> barrier.
 //
 // Same arithmetic per row, same colour order as the per-colour launches (k_gs_color_packed in packed.cu):
 // rows of one colour do not read each other (coloring.hpp:114-158), so the order of rows inside a colour is
 // free and the iterates are bit-identical (tests/test_gpu_cluster_sweep.py). The grid transfers ride on the
 // first and last step exactly as they do there (flags bit 0 / bit 1).
 //
-// Measured (tools/cluster_sweep_probe.py, tools/solve_sweep.py --sets cluster_rows=...): a phase costs 2.1-2.6 us,
-// i.e. what a launch costs — 64^3 solve 14.08 -> 13.84 ms with levels 2-3 on this path, 192^3 57.0 -> 58.8 ms.
-// The ncu source page puts the stall on ERRBAR/UCGABAR_WAIT: publishing z through GLOBAL memory makes every
-// `arrive.release` a device-wide memory barrier, which costs as much as the kernel boundary it replaces. The
-// version worth building keeps z in (distributed) shared memory, where the cluster barrier alone orders the
-// accesses. Until then the per-colour launches stay the default: tuning key "cluster_rows" = 0.
+// Measured (tools/solve_sweep.py --sets cluster_rows=0 cluster_rows=4096): no gain. First version, z in global
+// memory: 2.1-2.6 us per phase (64^3 solve 14.08 -> 13.84 ms, 192^3 57.0 -> 58.8 ms). This version, z in shared
+// memory: 64^3 14.09 -> 14.07 ms (levels 16^3 and 8^3), 104^3 20.2 -> 23.1 ms and 192^3 56.9 -> 58.2 ms (their 26^3 /
+// 24^3 levels: 16 CTAs, 67 us per sweep). The SASS says why: `barrier.cluster.arrive.release` — which is also what
+// cooperative groups' cluster.sync() emits — is MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR in front of UCGABAR_ARV, and
+// `wait.acquire` adds CCTL.IVALL: a device-wide memory barrier per phase whatever memory the data lives in, and
+// the ncu source page has the stall on exactly those instructions. That barrier costs what a kernel boundary
+// costs, so the 2.2 us "launch floor" of a colour step is really the price of publishing one colour's values.
+// The way past it: `arrive.relaxed` for the write-after-read edge only, and the values themselves
+// sent with st.async + mbarrier complete_tx, whose completion carries the ordering without a memory barrier.
+// Until that exists the per-colour launches stay the default: tuning key "cluster_rows" = 0.
 #include "kernels.cuh"
 
 #include <algorithm>
@@ -46,17 +52,32 @@ namespace slabgpu {
 
 			constexpr int kMaxSweepColors = 8;
 			constexpr int kMaxClusterCtas = 16;
-			constexpr int kMaxSweepSmem = 200 * 1024;
-
-			size_t sweep_smem_bytes( int ncolors, int chunks, unsigned int block ) {
-				return static_cast< size_t >( ncolors ) * block * ( 16u * chunks + 8u + 4u );
-			}
+			constexpr size_t kMaxSweepSmem = 220 * 1024;
 
 			struct SweepColors {
 				int32_t pos[ kMaxSweepColors ];   // first position of the colour in the colour-sorted matrix
 				int32_t count[ kMaxSweepColors ]; // members
 				int32_t ncolors;
+				int32_t n;                        // length of z
 			};
+
+			// cluster shape for a level: about 64 rows per CTA (a phase is a latency chain, not a throughput problem),
+			// power-of-two clusters, one row per thread
+			struct SweepShape {
+				unsigned int ctas, block;
+				size_t smem;
+			};
+			SweepShape sweep_shape( uint64_t largest, int ncolors, int chunks, uint64_t n ) {
+				SweepShape sh{};
+				sh.ctas = 1;
+				while( sh.ctas < static_cast< unsigned int >( kMaxClusterCtas ) && static_cast< uint64_t >( sh.ctas ) * 64u < largest ) {
+					sh.ctas *= 2;
+				}
+				const unsigned int per_cta = static_cast< unsigned int >( ( largest + sh.ctas - 1 ) / sh.ctas );
+				sh.block = std::max( 32u, ( per_cta + 31u ) / 32u * 32u );
+				sh.smem = static_cast< size_t >( ncolors ) * sh.block * ( 16u * chunks + 8u + 4u ) + 8u * n;
+				return sh;
+			}
 
 			__device__ __forceinline__ void cluster_arrive() {
 				asm volatile( "barrier.cluster.arrive.release;" ::: "memory" );
@@ -64,11 +85,20 @@ namespace slabgpu {
 			__device__ __forceinline__ void cluster_wait() {
 				asm volatile( "barrier.cluster.wait.acquire;" ::: "memory" );
 			}
+			// store v at the same shared-memory offset of CTA `rank` of the cluster
+			__device__ __forceinline__ void remote_store( uint32_t local_addr, unsigned int rank, double v ) {
+				uint32_t remote;
+				asm volatile( "mapa.shared::cluster.u32 %0, %1, %2;" : "=r"( remote ) : "r"( local_addr ), "r"( rank ) );
+				asm volatile( "st.shared::cluster.f64 [%0], %1;" :: "r"( remote ), "d"( v ) : "memory" );
+			}
 
-			// Shared memory of a CTA: what its rows need and the sweep does not change — codes, row index, r[i] — for
-			// every colour, one slot per thread: [colour][chunk][thread] uint4 | [colour][thread] double | [colour][thread] int32.
-			// Filled once in the prologue (the matrix part before the wait on the previous kernel), so that a phase is
-			// barrier -> one round of gathers from the L2 -> the row's add chain -> store -> barrier and nothing else.
+			// Shared memory of a CTA:
+			//   [colour][chunk][thread] uint4 | [colour][thread] double | [colour][thread] int32   the part of its rows' work that
+			//       the sweep does not change (codes, r[i], row index), filled once in the prologue — the matrix part before
+			//       the wait on the previous kernel;
+			//   [n] double   a full copy of z. Every CTA gathers from its own copy; a row's new value is stored into every
+			//       CTA's copy through distributed shared memory, and the cluster barrier between two colours orders those
+			//       stores against the next colour's gathers. Global memory sees z again only at the end.
 			extern __shared__ uint4 sweep_smem[];
 
 			// steps of the sweep: colours 0..nc-1, then nc-2..0; the step of colour nc-1 applies its update twice
@@ -80,12 +110,15 @@ namespace slabgpu {
 				const double * src, double * out, double * zero ) {
 				const int tx = static_cast< int >( threadIdx.x );
 				const int B = static_cast< int >( blockDim.x );
-				const int t = static_cast< int >( blockIdx.x ) * B + tx;
+				const unsigned int rank = blockIdx.x; // one cluster: the CTA's rank in it
+				const unsigned int ctas = gridDim.x;
+				const int t = static_cast< int >( rank ) * B + tx;
 				const int nc = sc.ncolors;
 				const int nsteps = 2 * nc - 1;
 				uint4 * s_codes = sweep_smem;
 				double * s_r = reinterpret_cast< double * >( s_codes + nc * CHUNKS * B );
 				int32_t * s_i = reinterpret_cast< int32_t * >( s_r + nc * B );
+				double * s_z = reinterpret_cast< double * >( s_i + nc * B );
 				{
 					// all loads of all colours go out together (unrolled: a rolled loop would wait for each colour's data
 					// before asking for the next)
@@ -119,6 +152,9 @@ namespace slabgpu {
 					for( int c = 0; c < kMaxSweepColors; ++c ) {
 						r_of[ c ] = c < nc && row_of[ c ] >= 0 ? r[ row_of[ c ] ] : 0.0;
 					}
+					for( int j = tx; j < sc.n; j += B ) {
+						s_z[ j ] = z[ j ];
+					}
 					#pragma unroll
 					for( int c = 0; c < kMaxSweepColors; ++c ) {
 						if( c < nc ) {
@@ -126,6 +162,9 @@ namespace slabgpu {
 						}
 					}
 				}
+				// every copy of z complete (and every CTA of the cluster running) before anybody stores into it
+				cluster_arrive();
+				cluster_wait();
 				#pragma unroll 1
 				for( int s = 0; s < nsteps; ++s ) {
 					const int c = s < nc ? s : nsteps - 1 - s;
@@ -141,30 +180,44 @@ namespace slabgpu {
 						const int flags = ( s == 0 ? first_flags : 0 ) | ( s == nsteps - 1 ? last_flags : 0 );
 						const int passes = s == nc - 1 ? 2 : 1;
 						const bool warp_ragged = __any_sync( __activemask(), rc.template ragged< NCODES >() );
-						double zi = z[ i ];
+						double zi = s_z[ i ];
 						if( flags & 1 ) { // multigrid.hpp:76-77 on the injected rows
 							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ t ] ) );
 							zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
-							z[ i ] = zi;
+							s_z[ i ] = zi;
 						}
 						#pragma unroll 1
 						for( int pass = 0; pass < passes; ++pass ) { // smoother.hpp:60-72
 							double d = 0.0;
-							const double sum = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, z, dp, d );
+							const double sum = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, s_z, dp, d );
 							zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
-							z[ i ] = zi;
+							s_z[ i ] = zi; // rows of the colour do not read each other: only this thread reads it before the barrier
 						}
 						if( flags & 2 ) { // multigrid.hpp:100-104 on the injected rows
 							double unused = 0.0;
-							const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, z, dp, unused );
+							const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, s_z, dp, unused );
 							const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
 							out[ t ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 							zero[ t ] = 0.0;
 						}
+						if( s + 1 < nsteps ) { // the other copies
+							const uint32_t at = static_cast< uint32_t >( __cvta_generic_to_shared( s_z + i ) );
+							for( unsigned int other = 0; other < ctas; ++other ) {
+								if( other != rank ) {
+									remote_store( at, other, zi );
+								}
+							}
+						}
 					}
-					if( s + 1 < nsteps ) {
-						cluster_arrive();
-						cluster_wait();
+					// also after the last step: no CTA may leave while others could still store into its shared memory
+					cluster_arrive();
+					cluster_wait();
+				}
+				#pragma unroll 1
+				for( int c = 0; c < nc; ++c ) {
+					const int32_t i = s_i[ c * B + tx ];
+					if( i >= 0 ) {
+						z[ i ] = s_z[ i ];
 					}
 				}
 			}
@@ -207,7 +260,7 @@ namespace slabgpu {
 
 			template< int N, int D >
 			void sweep_launch( cudaStream_t st, const Packed & P, const PlainRef & plain, const int32_t * rows, const SweepColors & sc,
-				unsigned int ctas, unsigned int block, double * z, const double * r, int first_flags, int last_flags,
+				unsigned int ctas, unsigned int block, size_t smem, double * z, const double * r, int first_flags, int last_flags,
 				const double * src, double * out, double * zero ) {
 				constexpr int C = ( N + 16 ) / 16;
 				constexpr int W = ( N + 3 ) / 4; // every gather of the row in flight at once: the phase is latency-bound
@@ -215,30 +268,31 @@ namespace slabgpu {
 				static bool large_clusters_allowed = false; // clusters of more than 8 CTAs are opt-in per kernel
 				if( !large_clusters_allowed ) {
 					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1 ) );
-					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSweepSmem ) );
+					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( kMaxSweepSmem ) ) );
 					large_clusters_allowed = true;
 				}
-				launch_cluster( kernel, ctas, block, sweep_smem_bytes( sc.ncolors, C, block ), st, P.codes, dict_param< D >( P ), plain, rows, sc, z, r, first_flags, last_flags,
+				launch_cluster( kernel, ctas, block, smem, st, P.codes, dict_param< D >( P ), plain, rows, sc, z, r, first_flags, last_flags,
 					src, out, zero );
 			}
 
 			template< int D >
 			void sweep_by_width( cudaStream_t st, const Packed & P, const PlainRef & plain, const int32_t * rows, const SweepColors & sc,
-				unsigned int ctas, unsigned int block, double * z, const double * r, int first_flags, int last_flags,
+				unsigned int ctas, unsigned int block, size_t smem, double * z, const double * r, int first_flags, int last_flags,
 				const double * src, double * out, double * zero ) {
 				switch( P.ncodes ) {
-					case 8: sweep_launch< 8, D >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero ); break;
-					case 16: sweep_launch< 16, D >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero ); break;
-					case 27: sweep_launch< 27, D >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero ); break;
-					case 32: sweep_launch< 32, D >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero ); break;
-					case 64: sweep_launch< 64, D >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero ); break;
+					case 8: sweep_launch< 8, D >( st, P, plain, rows, sc, ctas, block, smem, z, r, first_flags, last_flags, src, out, zero ); break;
+					case 16: sweep_launch< 16, D >( st, P, plain, rows, sc, ctas, block, smem, z, r, first_flags, last_flags, src, out, zero ); break;
+					case 27: sweep_launch< 27, D >( st, P, plain, rows, sc, ctas, block, smem, z, r, first_flags, last_flags, src, out, zero ); break;
+					case 32: sweep_launch< 32, D >( st, P, plain, rows, sc, ctas, block, smem, z, r, first_flags, last_flags, src, out, zero ); break;
+					case 64: sweep_launch< 64, D >( st, P, plain, rows, sc, ctas, block, smem, z, r, first_flags, last_flags, src, out, zero ); break;
 					default: fail( SLAB_ERR_INTERNAL, "packed matrix with an unknown width class" );
 				}
 			}
 
 		} // namespace
 
-		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size ) {
+		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size,
+			uint64_t n ) {
 			if( g_cluster_rows <= 0 || !g_use_packed || !S.packed.usable() ) {
 				return false;
 			}
@@ -248,34 +302,31 @@ namespace slabgpu {
 			}
 			const uint64_t largest = *std::max_element( color_size.begin(), color_size.end() );
 			const int64_t limit = std::min< int64_t >( g_cluster_rows, static_cast< int64_t >( kMaxClusterCtas ) * kBlock );
-			return largest >= 1 && static_cast< int64_t >( largest ) <= limit && color_pos[ nc - 1 ] < ( int64_t( 1 ) << 30 )
-				&& sweep_smem_bytes( static_cast< int >( nc ), S.packed.chunks, kBlock ) <= static_cast< size_t >( kMaxSweepSmem );
+			if( largest < 1 || static_cast< int64_t >( largest ) > limit || color_pos[ nc - 1 ] >= ( int64_t( 1 ) << 30 ) ) {
+				return false;
+			}
+			return sweep_shape( largest, static_cast< int >( nc ), S.packed.chunks, n ).smem <= kMaxSweepSmem; // z has to fit
 		}
 
 		void gs_sweep_cluster( cudaStream_t st, const Sell & S, const int32_t * rows, const std::vector< int64_t > & color_pos,
-			const std::vector< uint64_t > & color_size, double * z, const double * r, int first_flags, int last_flags,
+			const std::vector< uint64_t > & color_size, uint64_t n, double * z, const double * r, int first_flags, int last_flags,
 			const double * src, double * out, double * zero ) {
 			const Packed & P = S.packed;
 			const PlainRef plain{ S.slice_off, S.vals, S.cols };
 			SweepColors sc{};
 			sc.ncolors = static_cast< int32_t >( color_size.size() );
+			sc.n = static_cast< int32_t >( n );
 			uint64_t largest = 1;
 			for( int k = 0; k < sc.ncolors; ++k ) {
 				sc.pos[ k ] = static_cast< int32_t >( color_pos[ k ] );
 				sc.count[ k ] = static_cast< int32_t >( color_size[ k ] );
 				largest = std::max( largest, color_size[ k ] );
 			}
-			// spread thin (about 64 rows per CTA: the phase is a latency chain, not a throughput problem), power-of-two clusters
-			unsigned int ctas = 1;
-			while( ctas < static_cast< unsigned int >( kMaxClusterCtas ) && static_cast< uint64_t >( ctas ) * 64u < largest ) {
-				ctas *= 2;
-			}
-			const unsigned int per_cta = static_cast< unsigned int >( ( largest + ctas - 1 ) / ctas );
-			const unsigned int block = std::max( 32u, ( per_cta + 31u ) / 32u * 32u );
+			const SweepShape sh = sweep_shape( largest, sc.ncolors, P.chunks, n );
 			if( P.dict_size <= 32 ) {
-				sweep_by_width< 32 >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero );
+				sweep_by_width< 32 >( st, P, plain, rows, sc, sh.ctas, sh.block, sh.smem, z, r, first_flags, last_flags, src, out, zero );
 			} else {
-				sweep_by_width< 256 >( st, P, plain, rows, sc, ctas, block, z, r, first_flags, last_flags, src, out, zero );
+				sweep_by_width< 256 >( st, P, plain, rows, sc, sh.ctas, sh.block, sh.smem, z, r, first_flags, last_flags, src, out, zero );
 			}
 		}
 
