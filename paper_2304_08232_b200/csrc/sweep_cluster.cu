@@ -1,30 +1,34 @@
-// sweep_cluster.cu — a whole symmetric Gauss-Seidel sweep of a SMALL level in one launch (experiment, off by default).
+// sweep_cluster.cu — a whole symmetric Gauss-Seidel sweep of a SMALL level in one launch.
 //
 // Why. A colour step of a coarse level is a few hundred to a few thousand rows: its kernel runs at the floor
 // of a dependent launch (2.2 us on B200 inside a CUDA graph with programmatic launches), and a symmetric sweep
-// is fifteen of them (smoother.hpp:108-111). Here one thread-block cluster (up to 16 CTAs, one row per thread)
-// walks the colours of the sweep itself and separates them with the cluster's hardware barrier instead of a
-// kernel boundary. Everything a row needs that the sweep does not change — its codes, its row index, r[i] — sits
-// in shared memory from the prologue on, and so does z: every CTA holds a full copy, gathers from its own copy
-// and stores a row's new value into every copy through distributed shared memory. A phase is then
-// barrier -> shared-memory gathers -> the row's add chain and divide -> 16 stores -> barrier.
+// is fifteen of them (smoother.hpp:108-111). Here ONE launch walks the colours of the sweep itself. Everything a
+// row needs that the sweep does not change — its codes, its row index, r[i] — sits in shared memory from the
+// prologue on (the matrix part is fetched before the wait on the previous kernel), and so does z; a phase is
+// barrier -> shared-memory gathers -> the row's add chain and divide -> barrier. Global memory sees z again at
+// the end.
 //
 // Same arithmetic per row, same colour order as the per-colour launches (k_gs_color_packed in packed.cu):
 // rows of one colour do not read each other (coloring.hpp:114-158), so the order of rows inside a colour is
 // free and the iterates are bit-identical (tests/test_gpu_cluster_sweep.py). The grid transfers ride on the
 // first and last step exactly as they do there (flags bit 0 / bit 1).
 //
-// Measured (tools/solve_sweep.py --sets cluster_rows=0 cluster_rows=4096): no gain. First version, z in global
-// memory: 2.1-2.6 us per phase (64^3 solve 14.08 -> 13.84 ms, 192^3 57.0 -> 58.8 ms). This version, z in shared
-// memory: 64^3 14.09 -> 14.07 ms (levels 16^3 and 8^3), 104^3 20.2 -> 23.1 ms and 192^3 56.9 -> 58.2 ms (their 26^3 /
-// 24^3 levels: 16 CTAs, 67 us per sweep). The SASS says why: `barrier.cluster.arrive.release` — which is also what
-// cooperative groups' cluster.sync() emits — is MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR in front of UCGABAR_ARV, and
-// `wait.acquire` adds CCTL.IVALL: a device-wide memory barrier per phase whatever memory the data lives in, and
-// the ncu source page has the stall on exactly those instructions. That barrier costs what a kernel boundary
-// costs, so the 2.2 us "launch floor" of a colour step is really the price of publishing one colour's values.
-// The way past it: `arrive.relaxed` for the write-after-read edge only, and the values themselves
-// sent with st.async + mbarrier complete_tx, whose completion carries the ordering without a memory barrier.
-// Until that exists the per-colour launches stay the default: tuning key "cluster_rows" = 0.
+// Two modes, chosen by the level's largest colour (tuning key "cluster_rows", default 256):
+//  * one CTA (up to 512 rows per colour, one row per thread), __syncthreads between the colours. ON by default for
+//    colours of at most 256 rows: 16^3 4-level solve 10.6 -> 7.9 ms, 32^3 11.9 -> 10.3 ms, 64^3 14.3 -> 13.7 ms
+//    (tools/solve_sweep.py). One SM's constant-load and shared-memory throughput bounds a phase, so the gain is gone
+//    by ~350 rows per colour (13^3: no change) and at 512 it loses (64^3: 15.4 ms).
+//  * one thread-block cluster (up to 16 CTAs): every CTA holds a full copy of z, gathers from its own copy and
+//    stores a row's new value into every copy through distributed shared memory; the cluster barrier separates
+//    the colours. Correct, but no gain — measured with z in global memory first (2.1-2.6 us per phase; 64^3 14.08
+//    -> 13.84 ms, 192^3 57.0 -> 58.8 ms), then as described (104^3 20.2 -> 23.1 ms, 192^3 56.9 -> 58.2 ms for
+//    their 26^3 / 24^3 levels). The SASS says why: `barrier.cluster.arrive.release` — also what cooperative
+//    groups' cluster.sync() emits — is MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR in front of UCGABAR_ARV, and
+//    `wait.acquire` adds CCTL.IVALL: a device-wide memory barrier per phase wherever the data lives (the ncu
+//    source page has the stall on exactly those instructions). It costs what a kernel boundary costs, so the
+//    2.2 us "launch floor" of a colour step is really the price of publishing one colour's values. The way
+//    past it: `arrive.relaxed` for the write-after-read edge only, the values themselves sent
+//    with st.async + mbarrier complete_tx. Reached only when "cluster_rows" is raised above 512.
 #include "kernels.cuh"
 
 #include <algorithm>
@@ -39,9 +43,9 @@
 
 namespace slabgpu {
 
-	// largest colour (rows) of a level that takes the cluster sweep (at most 16 CTAs x 256 threads, one row per
-	// thread); 0 = off, the default (see above)
-	int64_t g_cluster_rows = 0;
+	// largest colour (rows) of a level that takes the one-launch sweep: up to 512 one CTA, above that (at most 4096)
+	// a cluster; 0 = per-colour launches everywhere. Default: the range where the one-CTA mode wins (see above).
+	int64_t g_cluster_rows = 256;
 
 	namespace kern {
 
@@ -52,6 +56,7 @@ namespace slabgpu {
 
 			constexpr int kMaxSweepColors = 8;
 			constexpr int kMaxClusterCtas = 16;
+			constexpr int kSingleBlock = 512;
 			constexpr size_t kMaxSweepSmem = 220 * 1024;
 
 			struct SweepColors {
@@ -70,7 +75,7 @@ namespace slabgpu {
 			SweepShape sweep_shape( uint64_t largest, int ncolors, int chunks, uint64_t n ) {
 				SweepShape sh{};
 				sh.ctas = 1;
-				while( sh.ctas < static_cast< unsigned int >( kMaxClusterCtas ) && static_cast< uint64_t >( sh.ctas ) * 64u < largest ) {
+				while( largest > static_cast< uint64_t >( kSingleBlock ) && sh.ctas < static_cast< unsigned int >( kMaxClusterCtas ) && static_cast< uint64_t >( sh.ctas ) * 64u < largest ) {
 					sh.ctas *= 2;
 				}
 				const unsigned int per_cta = static_cast< unsigned int >( ( largest + sh.ctas - 1 ) / sh.ctas );
@@ -84,6 +89,15 @@ namespace slabgpu {
 			}
 			__device__ __forceinline__ void cluster_wait() {
 				asm volatile( "barrier.cluster.wait.acquire;" ::: "memory" );
+			}
+			template< bool SINGLE >
+			__device__ __forceinline__ void phase_barrier() {
+				if( SINGLE ) {
+					__syncthreads();
+				} else {
+					cluster_arrive();
+					cluster_wait();
+				}
 			}
 			// store v at the same shared-memory offset of CTA `rank` of the cluster
 			__device__ __forceinline__ void remote_store( uint32_t local_addr, unsigned int rank, double v ) {
@@ -103,8 +117,10 @@ namespace slabgpu {
 
 			// steps of the sweep: colours 0..nc-1, then nc-2..0; the step of colour nc-1 applies its update twice
 			// (the last colour of the forward sweep is the first of the backward sweep, smoother.hpp:108-111)
-			template< int NCODES, int CHUNKS, int BATCH, int DICT >
-			__global__ void __launch_bounds__( kBlock ) k_gs_sweep_cluster( const uint4 * __restrict__ codes,
+			// SINGLE: the level fits one CTA (at most kSingleBlock rows per colour) — no cluster, no distributed stores, and
+			// the barrier between two colours is the CTA's own (BAR.SYNC, tens of cycles)
+			template< int NCODES, int CHUNKS, int BATCH, int DICT, bool SINGLE >
+			__global__ void __launch_bounds__( SINGLE ? kSingleBlock : kBlock ) k_gs_sweep_cluster( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows,
 				const __grid_constant__ SweepColors sc, double * z, const double * r, int first_flags, int last_flags,
 				const double * src, double * out, double * zero ) {
@@ -163,8 +179,7 @@ namespace slabgpu {
 					}
 				}
 				// every copy of z complete (and every CTA of the cluster running) before anybody stores into it
-				cluster_arrive();
-				cluster_wait();
+				phase_barrier< SINGLE >();
 				#pragma unroll 1
 				for( int s = 0; s < nsteps; ++s ) {
 					const int c = s < nc ? s : nsteps - 1 - s;
@@ -200,7 +215,7 @@ namespace slabgpu {
 							out[ t ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 							zero[ t ] = 0.0;
 						}
-						if( s + 1 < nsteps ) { // the other copies
+						if( !SINGLE && s + 1 < nsteps ) { // the other copies
 							const uint32_t at = static_cast< uint32_t >( __cvta_generic_to_shared( s_z + i ) );
 							for( unsigned int other = 0; other < ctas; ++other ) {
 								if( other != rank ) {
@@ -210,8 +225,7 @@ namespace slabgpu {
 						}
 					}
 					// also after the last step: no CTA may leave while others could still store into its shared memory
-					cluster_arrive();
-					cluster_wait();
+					phase_barrier< SINGLE >();
 				}
 				#pragma unroll 1
 				for( int c = 0; c < nc; ++c ) {
@@ -264,7 +278,18 @@ namespace slabgpu {
 				const double * src, double * out, double * zero ) {
 				constexpr int C = ( N + 16 ) / 16;
 				constexpr int W = ( N + 3 ) / 4; // every gather of the row in flight at once: the phase is latency-bound
-				auto kernel = k_gs_sweep_cluster< N, C, W, D >;
+				if( ctas == 1 ) {
+					auto kernel = k_gs_sweep_cluster< N, C, 2, D, true >; // 512 threads: the two-word batches' register count
+					static bool prepared = false;
+					if( !prepared ) {
+						SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( kMaxSweepSmem ) ) );
+						prepared = true;
+					}
+					launch_cluster( kernel, ctas, block, smem, st, P.codes, dict_param< D >( P ), plain, rows, sc, z, r, first_flags,
+						last_flags, src, out, zero );
+					return;
+				}
+				auto kernel = k_gs_sweep_cluster< N, C, W, D, false >;
 				static bool large_clusters_allowed = false; // clusters of more than 8 CTAs are opt-in per kernel
 				if( !large_clusters_allowed ) {
 					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1 ) );

@@ -1,5 +1,6 @@
-"""The one-launch cluster sweep (csrc/sweep_cluster.cu, tuning key cluster_rows; off by default) must give the
-bits of the per-colour launches and of the oracle: smoother.hpp:103-113, multigrid.hpp:87-116."""
+"""The one-launch sweep (csrc/sweep_cluster.cu, tuning key cluster_rows: one CTA up to 512 rows per colour — the
+default for small levels — and a thread-block cluster above) must give the bits of the per-colour launches and of
+the oracle: smoother.hpp:103-113, multigrid.hpp:87-116."""
 import json
 import os
 
@@ -17,7 +18,7 @@ def cluster_rows():
         _capi.set_tuning("cluster_rows", rows)
 
     yield apply
-    apply(0)
+    apply(256)  # the library default
 
 
 @pytest.mark.parametrize("dims", [(8, 8, 8), (16, 16, 16), (5, 7, 9), (26, 26, 26), (32, 32, 32), (3, 3, 3)])

@@ -22,8 +22,11 @@ def tune(slab):
         for key, value in {**DEFAULTS, **kw}.items():
             _capi.set_tuning(key, value)
 
+    # these tests are about the per-colour kernels: keep small levels off the one-launch sweep (sweep_cluster.cu)
+    _capi.set_tuning("cluster_rows", 0)
     yield apply
     apply()
+    _capi.set_tuning("cluster_rows", 256)
 
 
 # kernel shapes: (rows per thread of colour steps, of products, words per batch, block)
