@@ -75,7 +75,7 @@ int slab_set_programmatic_launch( int enabled );
  * "pack_build" (build it when a matrix is created, default 1), "keep_plain" (default 1; 0 frees the plain arrays of
  * matrices created afterwards whose coded copy has no escaped rows — 32 instead of 324 bytes per 27-point row, at the
  * price of download / transpose for those matrices), "packed_min_rows" (smaller launches use the plain arrays), "packed_batch", "packed_block", "packed_rows" / "packed_rows_spmv" (rows per thread of
- * colour steps / products), "packed_multi_min_rows"; "cluster_rows" (default 256: levels whose largest
+ * colour steps / products), "packed_multi_min_rows"; "cluster_rows" (default 384: levels whose largest
  * colour has at most this many rows run a whole symmetric sweep as ONE launch, csrc/sweep_cluster.cu — one CTA up to 512
  * rows, a thread-block cluster up to 4096, which is an experiment that does not pay; 0 = per-colour launches; env SLAB_CLUSTER_ROWS). Process-wide; each also has an environment variable
  * SLAB_<KEY> for the first four packed keys and the older ones. */

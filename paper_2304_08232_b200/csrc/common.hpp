@@ -71,7 +71,7 @@ namespace slabgpu {
 	extern int g_packed_rows;
 	extern int g_packed_rows_spmv;
 	extern int64_t g_packed_multi_min_rows;
-	extern int64_t g_cluster_rows;          // sweep_cluster.cu: largest colour of a level that takes the one-launch sweep (0 = off, default 256)
+	extern int64_t g_cluster_rows;          // sweep_cluster.cu: largest colour of a level that takes the one-launch sweep (0 = off, default 384)
 	extern int64_t g_packed_min_rows;
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;

@@ -13,11 +13,14 @@
 // free and the iterates are bit-identical (tests/test_gpu_cluster_sweep.py). The grid transfers ride on the
 // first and last step exactly as they do there (flags bit 0 / bit 1).
 //
-// Two modes, chosen by the level's largest colour (tuning key "cluster_rows", default 256):
+// Two modes, chosen by the level's largest colour (tuning key "cluster_rows", default 384):
 //  * one CTA (up to 512 rows per colour, one row per thread), __syncthreads between the colours. ON by default for
-//    colours of at most 256 rows: 16^3 4-level solve 10.6 -> 7.9 ms, 32^3 11.9 -> 10.3 ms, 64^3 14.3 -> 13.7 ms
-//    (tools/solve_sweep.py). One SM's constant-load and shared-memory throughput bounds a phase, so the gain is gone
-//    by ~350 rows per colour (13^3: no change) and at 512 it loses (64^3: 15.4 ms).
+//    colours of at most 384 rows: 16^3 4-level solve 10.6 -> 7.5 ms, 32^3 11.9 -> 10.0 ms, 64^3 14.3 -> 13.6 ms,
+//    104^3 20.2 -> 19.9 ms (tools/solve_sweep.py). The dictionary is copied to shared memory here: the rows of a
+//    small level are all boundary rows, a warp's codes differ, and constant loads with a different index per lane
+//    are replayed per distinct index (with the dictionary in the constant bank: 7.9 / 10.3 / 13.7 ms). One SM's
+//    shared-memory throughput bounds a phase (gathers 16 bytes apart are 4-way bank conflicts), so at 512 rows per
+//    colour the mode loses again (64^3: 14.6 ms).
 //  * one thread-block cluster (up to 16 CTAs): every CTA holds a full copy of z, gathers from its own copy and
 //    stores a row's new value into every copy through distributed shared memory; the cluster barrier separates
 //    the colours. Correct, but no gain — measured with z in global memory first (2.1-2.6 us per phase; 64^3 14.08
@@ -45,7 +48,7 @@ namespace slabgpu {
 
 	// largest colour (rows) of a level that takes the one-launch sweep: up to 512 one CTA, above that (at most 4096)
 	// a cluster; 0 = per-colour launches everywhere. Default: the range where the one-CTA mode wins (see above).
-	int64_t g_cluster_rows = 256;
+	int64_t g_cluster_rows = 384;
 
 	namespace kern {
 
@@ -131,6 +134,13 @@ namespace slabgpu {
 				const int t = static_cast< int >( rank ) * B + tx;
 				const int nc = sc.ncolors;
 				const int nsteps = 2 * nc - 1;
+				// the dictionary in shared memory: small levels are all boundary, the codes of a warp's rows differ, and
+				// constant loads with a different index per lane are replayed once per distinct index
+				__shared__ DictParam< DICT > s_dict;
+				for( int k = tx; k < DICT; k += B ) {
+					s_dict.e[ k ].val = dp.e[ k ].val;
+					s_dict.e[ k ].delta = dp.e[ k ].delta;
+				}
 				uint4 * s_codes = sweep_smem;
 				double * s_r = reinterpret_cast< double * >( s_codes + nc * CHUNKS * B );
 				int32_t * s_i = reinterpret_cast< int32_t * >( s_r + nc * B );
@@ -204,13 +214,13 @@ namespace slabgpu {
 						#pragma unroll 1
 						for( int pass = 0; pass < passes; ++pass ) { // smoother.hpp:60-72
 							double d = 0.0;
-							const double sum = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, s_z, dp, d );
+							const double sum = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, s_z, s_dict, d );
 							zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
 							s_z[ i ] = zi; // rows of the colour do not read each other: only this thread reads it before the barrier
 						}
 						if( flags & 2 ) { // multigrid.hpp:100-104 on the injected rows
 							double unused = 0.0;
-							const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, s_z, dp, unused );
+							const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, s_z, s_dict, unused );
 							const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
 							out[ t ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 							zero[ t ] = 0.0;

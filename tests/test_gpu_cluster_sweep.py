@@ -18,7 +18,7 @@ def cluster_rows():
         _capi.set_tuning("cluster_rows", rows)
 
     yield apply
-    apply(256)  # the library default
+    apply(384)  # the library default
 
 
 @pytest.mark.parametrize("dims", [(8, 8, 8), (16, 16, 16), (5, 7, 9), (26, 26, 26), (32, 32, 32), (3, 3, 3)])

@@ -26,7 +26,7 @@ def tune(slab):
     _capi.set_tuning("cluster_rows", 0)
     yield apply
     apply()
-    _capi.set_tuning("cluster_rows", 256)
+    _capi.set_tuning("cluster_rows", 384)
 
 
 # kernel shapes: (rows per thread of colour steps, of products, words per batch, block)
