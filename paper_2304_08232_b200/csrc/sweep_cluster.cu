@@ -15,12 +15,12 @@
 //
 // Two modes, chosen by the level's largest colour (tuning key "cluster_rows", default 384):
 //  * one CTA (up to 512 rows per colour, one row per thread), __syncthreads between the colours. ON by default for
-//    colours of at most 384 rows: 16^3 4-level solve 10.6 -> 7.5 ms, 32^3 11.9 -> 10.0 ms, 64^3 14.3 -> 13.6 ms,
-//    104^3 20.2 -> 19.9 ms (tools/solve_sweep.py). The dictionary is copied to shared memory here: the rows of a
-//    small level are all boundary rows, a warp's codes differ, and constant loads with a different index per lane
-//    are replayed per distinct index (with the dictionary in the constant bank: 7.9 / 10.3 / 13.7 ms). One SM's
-//    shared-memory throughput bounds a phase (gathers 16 bytes apart are 4-way bank conflicts), so at 512 rows per
-//    colour the mode loses again (64^3: 14.6 ms).
+//    colours of at most 384 rows: 16^3 4-level solve 10.6 -> 7.0 ms, 32^3 11.9 -> 9.7 ms, 64^3 14.3 -> 13.5 ms,
+//    104^3 20.2 -> 19.8 ms (tools/solve_sweep.py). The dictionary is copied to shared memory here, one 16-byte
+//    read per entry: the rows of a small level are all boundary rows, a warp's codes differ, and constant loads
+//    with a different index per lane are replayed per distinct index (dictionary in the constant bank: 7.9 /
+//    10.3 / 13.7 ms; in shared memory as two reads per entry and z unswizzled: 7.5 / 10.0 / 13.6 ms). One SM
+//    does the whole level, so at 512 rows per colour the mode only breaks even (64^3: 14.2 ms).
 //  * one thread-block cluster (up to 16 CTAs): every CTA holds a full copy of z, gathers from its own copy and
 //    stores a row's new value into every copy through distributed shared memory; the cluster barrier separates
 //    the colours. Correct, but no gain — measured with z in global memory first (2.1-2.6 us per phase; 64^3 14.08
@@ -83,7 +83,7 @@ namespace slabgpu {
 				}
 				const unsigned int per_cta = static_cast< unsigned int >( ( largest + sh.ctas - 1 ) / sh.ctas );
 				sh.block = std::max( 32u, ( per_cta + 31u ) / 32u * 32u );
-				sh.smem = static_cast< size_t >( ncolors ) * sh.block * ( 16u * chunks + 8u + 4u ) + 8u * n;
+				sh.smem = static_cast< size_t >( ncolors ) * sh.block * ( 16u * chunks + 8u + 4u ) + 8u * ( n + 2 ); // + 2: the swizzle may index one past an odd n
 				return sh;
 			}
 
@@ -107,6 +107,41 @@ namespace slabgpu {
 				uint32_t remote;
 				asm volatile( "mapa.shared::cluster.u32 %0, %1, %2;" : "=r"( remote ) : "r"( local_addr ), "r"( rank ) );
 				asm volatile( "st.shared::cluster.f64 [%0], %1;" :: "r"( remote ), "d"( v ) : "memory" );
+			}
+
+			// z in shared memory is stored swizzled: the rows of a colour are two elements apart, so the 16 lanes of a
+			// half-warp would hit only every other 8-byte slot of a 128-byte line (2-way conflicts on top of the two
+			// halves); flipping the lowest index bit in every other group of 16 spreads them over all slots.
+			__device__ __forceinline__ int swz( int j ) {
+				return j ^ ( ( j >> 4 ) & 1 );
+			}
+
+			// ordered row sum of a coded row (operations.hpp:116-125; same products, same order as coded_row_sum in
+			// packed_decode.cuh) from the shared-memory copies: one 16-byte read per dictionary entry, one swizzled
+			// 8-byte read per gathered element. Levels with escaped rows do not come here.
+			template< int NCODES, int CHUNKS >
+			__device__ __forceinline__ double sweep_row_sum( const RowCodes< CHUNKS > & rc, int32_t i, const double * s_z,
+				const uint4 * s_dict ) {
+				constexpr int WORDS = ( NCODES + 3 ) / 4;
+				double acc = 0.0;
+				#pragma unroll
+				for( int wi = 0; wi < WORDS; ++wi ) {
+					const unsigned int word = rc.word( wi );
+					#pragma unroll
+					for( int j = 0; j < 4; ++j ) {
+						if( 4 * wi + j < NCODES ) {
+							const unsigned int code = ( word >> ( 8 * j ) ) & 0xffu;
+							const uint4 e = s_dict[ code ];
+							const double val = __hiloint2double( static_cast< int >( e.y ), static_cast< int >( e.x ) );
+							const double xv = s_z[ swz( i + static_cast< int >( e.z ) ) ];
+							const double prod = __dmul_rn( val, xv );
+							if( code != 0u ) { // padding adds nothing
+								acc = __dadd_rn( acc, prod );
+							}
+						}
+					}
+				}
+				return acc;
 			}
 
 			// Shared memory of a CTA:
@@ -136,10 +171,11 @@ namespace slabgpu {
 				const int nsteps = 2 * nc - 1;
 				// the dictionary in shared memory: small levels are all boundary, the codes of a warp's rows differ, and
 				// constant loads with a different index per lane are replayed once per distinct index
-				__shared__ DictParam< DICT > s_dict;
+				__shared__ uint4 s_dict[ DICT ]; // {value low, value high, offset, -}
 				for( int k = tx; k < DICT; k += B ) {
-					s_dict.e[ k ].val = dp.e[ k ].val;
-					s_dict.e[ k ].delta = dp.e[ k ].delta;
+					const double v = dp.e[ k ].val;
+					s_dict[ k ] = make_uint4( static_cast< unsigned int >( __double2loint( v ) ), static_cast< unsigned int >( __double2hiint( v ) ),
+						static_cast< unsigned int >( dp.e[ k ].delta ), 0u );
 				}
 				uint4 * s_codes = sweep_smem;
 				double * s_r = reinterpret_cast< double * >( s_codes + nc * CHUNKS * B );
@@ -179,7 +215,7 @@ namespace slabgpu {
 						r_of[ c ] = c < nc && row_of[ c ] >= 0 ? r[ row_of[ c ] ] : 0.0;
 					}
 					for( int j = tx; j < sc.n; j += B ) {
-						s_z[ j ] = z[ j ];
+						s_z[ swz( j ) ] = z[ j ];
 					}
 					#pragma unroll
 					for( int c = 0; c < kMaxSweepColors; ++c ) {
@@ -201,32 +237,30 @@ namespace slabgpu {
 							rc.q[ j ] = s_codes[ ( c * CHUNKS + j ) * B + tx ];
 						}
 						const double ri = s_r[ c * B + tx ];
-						const int32_t pos = sc.pos[ c ] + t;
 						const int flags = ( s == 0 ? first_flags : 0 ) | ( s == nsteps - 1 ? last_flags : 0 );
 						const int passes = s == nc - 1 ? 2 : 1;
-						const bool warp_ragged = __any_sync( __activemask(), rc.template ragged< NCODES >() );
-						double zi = s_z[ i ];
+						double zi = s_z[ swz( i ) ];
 						if( flags & 1 ) { // multigrid.hpp:76-77 on the injected rows
 							const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, src[ t ] ) );
 							zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
-							s_z[ i ] = zi;
+							s_z[ swz( i ) ] = zi;
 						}
+						const uint4 de = s_dict[ rc.diag_code() ];
+						const double d = __hiloint2double( static_cast< int >( de.y ), static_cast< int >( de.x ) );
 						#pragma unroll 1
 						for( int pass = 0; pass < passes; ++pass ) { // smoother.hpp:60-72
-							double d = 0.0;
-							const double sum = any_row_sum< NCODES, CHUNKS, BATCH, true >( rc, warp_ragged, plain, pos, i, s_z, s_dict, d );
+							const double sum = sweep_row_sum< NCODES, CHUNKS >( rc, i, s_z, s_dict );
 							zi = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -sum ), __dmul_rn( zi, d ) ), d );
-							s_z[ i ] = zi; // rows of the colour do not read each other: only this thread reads it before the barrier
+							s_z[ swz( i ) ] = zi; // rows of the colour do not read each other: only this thread reads it before the barrier
 						}
 						if( flags & 2 ) { // multigrid.hpp:100-104 on the injected rows
-							double unused = 0.0;
-							const double az = any_row_sum< NCODES, CHUNKS, BATCH, false >( rc, warp_ragged, plain, pos, i, s_z, s_dict, unused );
+							const double az = sweep_row_sum< NCODES, CHUNKS >( rc, i, s_z, s_dict );
 							const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
 							out[ t ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
 							zero[ t ] = 0.0;
 						}
 						if( !SINGLE && s + 1 < nsteps ) { // the other copies
-							const uint32_t at = static_cast< uint32_t >( __cvta_generic_to_shared( s_z + i ) );
+							const uint32_t at = static_cast< uint32_t >( __cvta_generic_to_shared( s_z + swz( i ) ) );
 							for( unsigned int other = 0; other < ctas; ++other ) {
 								if( other != rank ) {
 									remote_store( at, other, zi );
@@ -241,7 +275,7 @@ namespace slabgpu {
 				for( int c = 0; c < nc; ++c ) {
 					const int32_t i = s_i[ c * B + tx ];
 					if( i >= 0 ) {
-						z[ i ] = s_z[ i ];
+						z[ i ] = s_z[ swz( i ) ];
 					}
 				}
 			}
@@ -328,7 +362,7 @@ namespace slabgpu {
 
 		bool gs_sweep_cluster_usable( const Sell & S, const std::vector< int64_t > & color_pos, const std::vector< uint64_t > & color_size,
 			uint64_t n ) {
-			if( g_cluster_rows <= 0 || !g_use_packed || !S.packed.usable() ) {
+			if( g_cluster_rows <= 0 || !g_use_packed || !S.packed.usable() || S.packed.escaped_rows != 0 ) {
 				return false;
 			}
 			const size_t nc = color_size.size();
