@@ -64,7 +64,8 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "smsp__inst_executed.sum",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_tensor.sum"]
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_tensor.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
 def full_capture(rep, label, traffic_key, traffic):
@@ -110,6 +111,9 @@ def main():
     # the dictionary-coded kernels (packed.cu): what bench.py's roofline.traffic reads
     full_capture("r01_gs_packed_192.ncu-rep", "r01_ncu_gs_packed_192.txt", ("gs_color_step", "192x192x192"), traffic)
     full_capture("r01_spmv_packed_192.ncu-rep", "r01_ncu_spmv_packed_192.txt", ("spmv", "192x192x192"), traffic)
+    # the one-launch sweep of a small level (sweep_cluster.cu), eager launch of tools/cluster_sweep_once.py
+    full_capture("r01_gs_sweep_8.ncu-rep", "r01_ncu_gs_sweep_8.txt", ("gs_sweep", "8x8x8"), traffic)
+    full_capture("r01_gs_sweep_13.ncu-rep", "r01_ncu_gs_sweep_13.txt", ("gs_sweep", "13x13x13"), traffic)
     with open(tpath, "w") as fh:
         json.dump(traffic, fh, indent=1)
     print(json.dumps(traffic))
