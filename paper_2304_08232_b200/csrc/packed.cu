@@ -399,7 +399,7 @@ namespace slabgpu {
 
 			// k_gs_color_packed with R rows per thread; covers the contiguous range [pos_begin, pos_begin + pos_count)
 			template< int NCODES, int CHUNKS, int R, int DICT >
-			__global__ void __launch_bounds__( kBlock, GS_MULTI_MINBLOCKS ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
+			__global__ void __launch_bounds__( kBlock, R == 2 ? GS_MULTI_MINBLOCKS : ( R == 3 ? 3 : 2 ) ) k_gs_color_packed_multi( const uint4 * __restrict__ codes,
 				const __grid_constant__ DictParam< DICT > dp, PlainRef plain, const int32_t * __restrict__ rows, int stride,
 				int64_t pos_begin, int64_t pos_count, double * z, const double * r, int flags,
 				const double * src, double * out, double * zero ) {
