@@ -140,6 +140,8 @@ typedef struct slab_format_info {
 	int64_t escaped_rows;   /* rows with an entry outside the dictionary: read from the plain arrays */
 	uint64_t plain_bytes;   /* bytes of the plain arrays */
 	uint64_t packed_bytes;  /* bytes of the coded copy */
+	uint64_t mask_bytes;    /* bytes of the 27-offset row masks (4 per row) that the shared-memory-staged kernels read on
+	                           box-shaped levels of a single-process context; 0 when the matrix has none */
 } slab_format_info;
 int slab_mat_format_info( slab_mat_t A, slab_format_info * out );
 

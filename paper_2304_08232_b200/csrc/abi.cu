@@ -107,6 +107,16 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_packed_batch = static_cast< int >( value );
 		} else if( k == "packed_min_rows" ) {
 			g_packed_min_rows = value;
+		} else if( k == "tile" ) {
+			g_use_tile = value ? 1 : 0;
+		} else if( k == "tile_min_rows" ) {
+			g_tile_min_rows = value;
+		} else if( k == "tile_ty" ) {
+			g_tile_ty = static_cast< int >( value );
+		} else if( k == "tile_cz" ) {
+			g_tile_cz = static_cast< int >( value );
+		} else if( k == "tile_ns" ) {
+			g_tile_ns = static_cast< int >( value );
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
 		} else if( k == "halo_overlap" ) {
@@ -274,6 +284,9 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		}
 		if( const char * v = std::getenv( "SLAB_STREAM_VARIANT" ) ) {
 			g_stream_variant = std::atoi( v );
+		}
+		if( const char * v = std::getenv( "SLAB_TILE" ) ) {
+			g_use_tile = std::atoi( v ) ? 1 : 0;
 		}
 		if( const char * v = std::getenv( "SLAB_PACKED" ) ) {
 			g_use_packed = std::atoi( v ) ? 1 : 0;
@@ -651,7 +664,8 @@ int slab_mat_device_bytes( slab_mat_t A, uint64_t * bytes ) {
 }
 
 namespace {
-	void fill_format_info( const Sell & S, slab_format_info * out ) {
+	void fill_format_info( const Sell & S, const BoxTile & T, slab_format_info * out ) {
+		out->mask_bytes = T.usable() ? static_cast< uint64_t >( S.nslices ) * kSlice * sizeof( uint32_t ) : 0u;
 		out->packed = S.packed.usable() ? 1 : 0;
 		out->width_class = S.packed.ncodes;
 		out->dict_size = S.packed.dict_size;
@@ -666,7 +680,7 @@ int slab_mat_format_info( slab_mat_t A, slab_format_info * out ) {
 	return guarded( [ & ] {
 		need( A, "slab_mat_format_info" );
 		need( out, "slab_mat_format_info" );
-		fill_format_info( A->sell, out );
+		fill_format_info( A->sell, A->tile, out );
 	} );
 }
 
@@ -674,7 +688,7 @@ int slab_level_format_info( slab_level_t level, slab_format_info * out ) {
 	return guarded( [ & ] {
 		need( level, "slab_level_format_info" );
 		need( out, "slab_level_format_info" );
-		fill_format_info( level->colorA, out );
+		fill_format_info( level->colorA, level->tile, out );
 	} );
 }
 

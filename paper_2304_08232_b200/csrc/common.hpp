@@ -73,6 +73,9 @@ namespace slabgpu {
 	extern int64_t g_packed_multi_min_rows;
 	extern int64_t g_cluster_rows;          // sweep_cluster.cu: largest colour of a level that takes the one-launch sweep (0 = off, default 384)
 	extern int64_t g_packed_min_rows;
+	extern int g_use_tile;            // tile.cu: shared-memory-staged kernels on stencil boxes (default 1)
+	extern int64_t g_tile_min_rows;   // ... for colour pairs / products of at least this many rows
+	extern int g_tile_ty, g_tile_cz, g_tile_ns; // tile shape overrides (0 = automatic)
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
 	}
@@ -128,6 +131,22 @@ namespace slabgpu {
 		}
 		uint64_t packed_bytes() const {
 			return packed.usable() ? static_cast< uint64_t >( nslices ) * packed.chunks * kSlice * 16u + 256u * 16u : 0u;
+		}
+	};
+
+	// Bitmap-coded companion of a coded matrix whose rows live on a 3D box (tile.cu). When every (column - row,
+	// value) pair of the dictionary is one of the 27 offsets dx + lx*(dy + ly*dz), |d| <= 1, with ONE value per
+	// offset, a row is the subset of those 27 pairs it stores: a 32-bit mask (bit 9*(dz+1) + 3*(dy+1) + (dx+1)),
+	// built from the row's codes and checked entry by entry when the matrix is created. Ascending bit order is
+	// ascending column order, so the ordered row sum of operations.hpp:116-125 walks the set bits. 4 bytes per
+	// row instead of 32; the kernels that read it stage the vector through shared memory with bulk-async copies.
+	struct BoxTile {
+		uint32_t * masks = nullptr; // device, one per row position (0 on padding positions)
+		double vals[ 27 ] = { 0.0 };  // the value of each offset (0.0: offset not in the dictionary)
+		int lx = 0, ly = 0, lz = 0;
+		void release();
+		bool usable() const {
+			return masks != nullptr;
 		}
 	};
 
@@ -191,6 +210,7 @@ struct slab_mat_s {
 	uint64_t nrows = 0, ncols = 0, nnz = 0;
 	slabgpu::Sell sell;             // natural row order
 	slabgpu::HaloPlan * plan = nullptr; // borrowed from the level: columns >= ncols are ghost slots
+	slabgpu::BoxTile tile;          // optional (stencil boxes on one process): natural-order rows as masks, tile.cu
 	std::unique_ptr< slab_mat_s > transposed; // built lazily for SLAB_DESC_TRANSPOSE
 	// host CSR kept when the matrix came from slab_mat_create_csr (small, test-sized inputs)
 	std::vector< uint64_t > h_row_offsets, h_cols;
@@ -219,6 +239,7 @@ struct slab_level_s {
 	bool is_stencil = false;
 	std::unique_ptr< slab_mat_s > A;       // natural-order SELL
 	slabgpu::Sell colorA;                  // colour-major SELL (positions)
+	slabgpu::BoxTile tile;                 // optional: colour-major rows as masks (tile.cu)
 	int32_t * d_rows = nullptr;            // position -> natural row, -1 on padding
 	slabgpu::Decomp decomp{};              // owned box of this rank on this level (whole grid when not distributed)
 	slabgpu::HaloPlan * plan = nullptr;    // owned; null on single-process contexts and general levels
@@ -293,6 +314,12 @@ namespace slabgpu {
 	// owned_cols: columns from this index on are ghost slots (never offered to the dictionary); < 0: none
 	void sell_pack( slab_ctx_s * ctx, Sell & S, const int32_t * d_rows, int64_t owned_cols = -1 );
 	Decomp single_domain( uint64_t nx, uint64_t ny, uint64_t nz );
+	// tile.cu: build T from the coded copy of S (rows: position -> natural row, nullptr = identity) on the box D;
+	// leaves T unusable when the matrix is not a subset-of-27-offsets matrix on that box
+	void box_tile_build( slab_ctx_s * ctx, const Sell & S, const int32_t * d_rows, const Decomp & D, BoxTile & T );
+	// is d_rows the parity lattice of the box (colour c = px + 2 py + 4 pz, members x-fastest)? The colour-pair
+	// kernel computes row positions from coordinates instead of reading the list.
+	bool box_tile_lattice_ok( slab_ctx_s * ctx, const int32_t * d_rows, const std::vector< int64_t > & color_pos, const Decomp & D );
 
 	// ---- dist.cu (3D domain decomposition, halo exchange, allreduce)
 	Decomp level_decomp( const slab_ctx_s * ctx, uint64_t lx, uint64_t ly, uint64_t lz ); // owned box of this rank

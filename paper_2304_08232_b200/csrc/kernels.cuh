@@ -11,6 +11,7 @@
 namespace slabgpu {
 	struct Decomp;
 	struct Sell;
+	struct BoxTile;
 	namespace kern {
 
 		// ---- vector ops (operations.hpp:49-106)
@@ -73,6 +74,14 @@ namespace slabgpu {
 			const int32_t * pos_list, const uint8_t * skip );
 		void residual_restrict_packed( cudaStream_t st, const Sell & S, const int32_t * rows, int64_t n_coarse,
 			const double * z, const double * r, double * r_c, double * zero );
+
+		// ---- tile.cu: shared-memory-staged kernels for matrices on a 3D box (BoxTile, common.hpp)
+		// the colours (2 pair, 2 pair + 1) of a stencil level in ONE launch; mode 0: forward order, 1: backward,
+		// 2: the turnaround of a symmetric sweep (even, odd, odd, even). flags as gs_color_step, on colour 0 only:
+		// bit 0 with mode 0, bit 1 with mode 1. Bit-identical to the colour-by-colour steps.
+		bool gs_pair_tile_usable( const BoxTile & T, int64_t pair_rows );
+		void gs_pair_tile( cudaStream_t st, int sm_count, const BoxTile & T, const std::vector< int64_t > & color_pos, int pair, int mode,
+			double * z, const double * r, int flags, const double * src, double * out, double * zero );
 
 		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
 		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a

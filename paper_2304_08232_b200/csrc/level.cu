@@ -9,6 +9,7 @@
 
 slab_level_s::~slab_level_s() {
 	colorA.release();
+	tile.release();
 	if( d_rows ) {
 		cudaFree( d_rows );
 	}
@@ -181,6 +182,12 @@ namespace slabgpu {
 			}
 			L->colorA = sell_stencil27( ctx, D, L->d_rows, npos );
 			sell_pack( ctx, L->colorA, L->d_rows, static_cast< int64_t >( L->n ) ); // columns >= n are ghost slots
+			// rows as masks over the 27 offsets, for the shared-memory-staged colour-pair kernel (tile.cu): single
+			// process only (no ghost columns), and only if the row list is the parity lattice that kernel assumes
+			if( ctx->dist == nullptr && D.n_ghost == 0 && L->colorA.packed.usable() && ( D.l[ 0 ] % 2 ) == 0
+				&& box_tile_lattice_ok( ctx, L->d_rows, L->color_pos, D ) ) {
+				box_tile_build( ctx, L->colorA, L->d_rows, D, L->tile );
+			}
 			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
 			uint64_t n_coarse = 0;
 			if( with_restriction ) {
@@ -378,13 +385,36 @@ namespace slabgpu {
 			}
 		}
 
+		// the colour-pair kernel of tile.cu serves this level? (stencil level on one process, masks built and checked)
+		bool tile_pairs_usable( const slab_level_s * L ) {
+			return L->is_stencil && L->plan == nullptr && L->num_colors == 8
+				&& kern::gs_pair_tile_usable( L->tile, static_cast< int64_t >( L->color_size[ 0 ] + L->color_size[ 1 ] ) );
+		}
+
+		void tile_pair_enqueue( slab_level_s * L, int pair, int mode, slab_vec_s * z, slab_vec_s * r, int flags ) {
+			kern::gs_pair_tile( L->ctx->stream, L->ctx->sm_count, L->tile, L->color_pos, pair, mode, z->d, r->d, flags,
+				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr );
+		}
+
 		void forward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:80-82
+			if( tile_pairs_usable( L ) ) {
+				for( int p = 0; p < 4; ++p ) {
+					tile_pair_enqueue( L, p, 0, z, r, 0 );
+				}
+				return;
+			}
 			for( uint64_t k = 0; k < L->num_colors; ++k ) {
 				color_step_enqueue( L, k, z, r );
 			}
 		}
 
 		void backward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:95-97
+			if( tile_pairs_usable( L ) ) {
+				for( int p = 3; p >= 0; --p ) {
+					tile_pair_enqueue( L, p, 1, z, r, 0 );
+				}
+				return;
+			}
 			for( uint64_t k = L->num_colors; k > 0; --k ) {
 				color_step_enqueue( L, k - 1, z, r );
 			}
@@ -406,6 +436,23 @@ namespace slabgpu {
 				kern::gs_sweep_cluster( L->ctx->stream, L->colorA, L->d_rows, L->color_pos, L->color_size, L->n, z->d, r->d,
 					first_flags, last_flags, ( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr,
 					( flags & 2 ) ? L->z_c->d : nullptr );
+				return;
+			}
+			if( tile_pairs_usable( L ) ) {
+				// colour pairs (2p, 2p+1) as single launches (tile.cu); 7 launches per symmetric sweep with the turnaround
+				const bool turn = L->ctx->fused_transfers != 0;
+				for( int p = 0; p < 3; ++p ) {
+					tile_pair_enqueue( L, p, 0, z, r, p == 0 ? first_flags : 0 );
+				}
+				if( turn ) {
+					tile_pair_enqueue( L, 3, 2, z, r, 0 );
+				} else {
+					tile_pair_enqueue( L, 3, 0, z, r, 0 );
+					tile_pair_enqueue( L, 3, 1, z, r, 0 );
+				}
+				for( int p = 2; p >= 0; --p ) {
+					tile_pair_enqueue( L, p, 1, z, r, p == 0 ? last_flags : 0 );
+				}
 				return;
 			}
 			const bool turnaround = L->ctx->fused_transfers && nc >= 2
