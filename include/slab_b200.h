@@ -142,6 +142,10 @@ typedef struct slab_format_info {
 	uint64_t packed_bytes;  /* bytes of the coded copy */
 	uint64_t mask_bytes;    /* bytes of the 27-offset row masks (4 per row) that the shared-memory-staged kernels read on
 	                           box-shaped levels of a single-process context; 0 when the matrix has none */
+	int32_t plane_phases;   /* 1 when the matrix is a regular 27-point box operator (one value per offset, every row
+	                           storing exactly its in-box offsets): sweeps and products then run from zero-padded
+	                           plane slabs in shared memory and read no matrix stream at all */
+	int32_t reserved;
 } slab_format_info;
 int slab_mat_format_info( slab_mat_t A, slab_format_info * out );
 

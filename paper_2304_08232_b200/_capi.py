@@ -83,7 +83,7 @@ class _CgResult(C.Structure):
 class FormatInfo(C.Structure):  # slab_format_info
     _fields_ = [("packed", C.c_int32), ("width_class", C.c_int32), ("dict_size", C.c_int32), ("stride", C.c_int32),
                 ("escaped_rows", C.c_int64), ("plain_bytes", C.c_uint64), ("packed_bytes", C.c_uint64),
-                ("mask_bytes", C.c_uint64)]
+                ("mask_bytes", C.c_uint64), ("plane_phases", C.c_int32), ("reserved", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

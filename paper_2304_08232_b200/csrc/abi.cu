@@ -117,6 +117,18 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_tile_cz = static_cast< int >( value );
 		} else if( k == "tile_ns" ) {
 			g_tile_ns = static_cast< int >( value );
+		} else if( k == "planes" ) {
+			g_use_planes = value ? 1 : 0;
+		} else if( k == "plane_min_rows" ) {
+			g_plane_min_rows = value;
+		} else if( k == "plane_ty" ) {
+			g_plane_ty = static_cast< int >( value );
+		} else if( k == "plane_cz" ) {
+			g_plane_cz = static_cast< int >( value );
+		} else if( k == "plane_ns" ) {
+			g_plane_ns = static_cast< int >( value );
+		} else if( k == "plane_rows" ) {
+			g_plane_rows = static_cast< int >( value );
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
 		} else if( k == "halo_overlap" ) {
@@ -666,6 +678,8 @@ int slab_mat_device_bytes( slab_mat_t A, uint64_t * bytes ) {
 namespace {
 	void fill_format_info( const Sell & S, const BoxTile & T, slab_format_info * out ) {
 		out->mask_bytes = T.usable() ? static_cast< uint64_t >( S.nslices ) * kSlice * sizeof( uint32_t ) : 0u;
+		out->plane_phases = T.usable() && T.regular ? 1 : 0;
+		out->reserved = 0;
 		out->packed = S.packed.usable() ? 1 : 0;
 		out->width_class = S.packed.ncodes;
 		out->dict_size = S.packed.dict_size;
@@ -689,6 +703,7 @@ int slab_level_format_info( slab_level_t level, slab_format_info * out ) {
 		need( level, "slab_level_format_info" );
 		need( out, "slab_level_format_info" );
 		fill_format_info( level->colorA, level->tile, out );
+		out->plane_phases = level->planes_ok ? 1 : 0;
 	} );
 }
 

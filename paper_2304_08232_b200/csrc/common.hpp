@@ -76,6 +76,9 @@ namespace slabgpu {
 	extern int g_use_tile;            // tile.cu: shared-memory-staged kernels on stencil boxes (default 1)
 	extern int64_t g_tile_min_rows;   // ... for colour pairs / products of at least this many rows
 	extern int g_tile_ty, g_tile_cz, g_tile_ns; // tile shape overrides (0 = automatic)
+	extern int g_use_planes;          // plane.cu: three-launch symmetric sweeps on regular box levels (default 1)
+	extern int64_t g_plane_min_rows;  // ... for levels of at least this many rows
+	extern int g_plane_ty, g_plane_cz, g_plane_ns, g_plane_rows; // shape overrides (0 = automatic)
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
 	}
@@ -144,6 +147,9 @@ namespace slabgpu {
 		uint32_t * masks = nullptr; // device, one per row position (0 on padding positions)
 		double vals[ 27 ] = { 0.0 };  // the value of each offset (0.0: offset not in the dictionary)
 		int lx = 0, ly = 0, lz = 0;
+		// every row stores exactly the offsets that stay inside the box, all 27 values are finite: the kernels of
+		// plane.cu need no masks then (zero-padded slabs stand in for the absent neighbours)
+		bool regular = false;
 		void release();
 		bool usable() const {
 			return masks != nullptr;
@@ -251,6 +257,8 @@ struct slab_level_s {
 	std::unique_ptr< slab_mat_s > R;       // restriction (n_c x n), null at the coarsest
 	std::unique_ptr< slab_level_s > coarser;
 	std::unique_ptr< slab_vec_s > s, f, r_c, z_c; // scratch (problem.hpp:228-231)
+	std::unique_ptr< slab_vec_s > zs;             // plane.cu: the out-of-place partner of the smoothed vector
+	bool planes_ok = false;                       // the level can run the plane phases of plane.cu
 	slab_level_stats stats{};
 	// V-cycle graph cache (keyed by the vectors it was captured with)
 	cudaGraphExec_t vcycle_exec = nullptr;

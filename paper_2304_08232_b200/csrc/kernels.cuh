@@ -83,6 +83,18 @@ namespace slabgpu {
 		void gs_pair_tile( cudaStream_t st, int sm_count, const BoxTile & T, const std::vector< int64_t > & color_pos, int pair, int mode,
 			double * z, const double * r, int flags, const double * src, double * out, double * zero );
 
+		// ---- plane.cu: a symmetric sweep of a regular box level as three plane phases (even planes: colours 0-3; odd
+		// planes: colours 4-7 and 7-4; even planes: colours 3-0), every phase out of place, the vector staged through
+		// shared memory by bulk-async copies. kind: 0 = colours 0..3, 1 = 4..7,7..4, 2 = 3..0, 3 = 4..7, 4 = 7..4.
+		// own_in / nb_in: where the planes of the phase's parity / their neighbour planes are read from; own_out: where
+		// the updated planes go (not own_in); pass (bit 0: plane z+1, bit 1: plane z-1, bit 2: plane z+1 if it is the
+		// last of the box): neighbour planes copied through to pass_out. flags / src / out / zero as gs_color_step,
+		// bit 0 with kind 0, bit 1 with kind 2. Bit-identical to the colour-by-colour steps.
+		bool gs_planes_usable( const BoxTile & T, int64_t rows, int sm_count );
+		void gs_planes_prepare(); // function attributes; call outside stream capture
+		void gs_planes( cudaStream_t st, int sm_count, const BoxTile & T, int kind, int pass, const double * own_in, const double * nb_in,
+			double * own_out, double * pass_out, const double * r, int flags, const double * src, double * out, double * zero );
+
 		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
 		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a
 		// kernel launch (coarse levels are launch-latency-bound). Same arithmetic, same order.

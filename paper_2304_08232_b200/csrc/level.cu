@@ -187,6 +187,11 @@ namespace slabgpu {
 			if( ctx->dist == nullptr && D.n_ghost == 0 && L->colorA.packed.usable() && ( D.l[ 0 ] % 2 ) == 0
 				&& box_tile_lattice_ok( ctx, L->d_rows, L->color_pos, D ) ) {
 				box_tile_build( ctx, L->colorA, L->d_rows, D, L->tile );
+				if( L->tile.usable() && kern::gs_planes_usable( L->tile, 0, ctx->sm_count ) ) {
+					L->planes_ok = true;
+					L->zs.reset( vec_new( ctx, L->n, 0.0 ) );
+					kern::gs_planes_prepare();
+				}
 			}
 			L->a_diag.reset( vec_new( ctx, L->n, 26.0 ) ); // extract_diagonal of the stencil: 26.0 everywhere
 			uint64_t n_coarse = 0;
@@ -396,7 +401,24 @@ namespace slabgpu {
 				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr );
 		}
 
+		// the three-launch plane phases of plane.cu serve this level? (regular stencil box on one process)
+		bool planes_usable( const slab_level_s * L ) {
+			return L->planes_ok && g_use_planes && L->plan == nullptr && static_cast< int64_t >( L->n ) >= g_plane_min_rows;
+		}
+
+		void plane_phase_enqueue( slab_level_s * L, int kind, int pass, const double * own_in, const double * nb_in, double * own_out,
+			double * pass_out, slab_vec_s * r, int flags ) {
+			kern::gs_planes( L->ctx->stream, L->ctx->sm_count, L->tile, kind, pass, own_in, nb_in, own_out, pass_out, r->d, flags,
+				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr );
+		}
+
 		void forward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:80-82
+			if( planes_usable( L ) ) {
+				double * const zs = L->zs->d;
+				plane_phase_enqueue( L, 0, 1, z->d, z->d, zs, zs, r, 0 );     // colours 0..3: z -> zs, odd planes copied along
+				plane_phase_enqueue( L, 3, 2 | 4, zs, zs, z->d, z->d, r, 0 ); // colours 4..7: zs -> z, even planes copied along
+				return;
+			}
 			if( tile_pairs_usable( L ) ) {
 				for( int p = 0; p < 4; ++p ) {
 					tile_pair_enqueue( L, p, 0, z, r, 0 );
@@ -409,6 +431,12 @@ namespace slabgpu {
 		}
 
 		void backward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:95-97
+			if( planes_usable( L ) ) {
+				double * const zs = L->zs->d;
+				plane_phase_enqueue( L, 4, 2 | 4, z->d, z->d, zs, zs, r, 0 ); // colours 7..4: z -> zs, even planes copied along
+				plane_phase_enqueue( L, 2, 1, zs, zs, z->d, z->d, r, 0 );     // colours 3..0: zs -> z, odd planes copied along
+				return;
+			}
 			if( tile_pairs_usable( L ) ) {
 				for( int p = 3; p >= 0; --p ) {
 					tile_pair_enqueue( L, p, 1, z, r, 0 );
@@ -429,6 +457,14 @@ namespace slabgpu {
 		// first_flags / last_flags ride on the first forward and the last backward step (grid transfers).
 		void sweep_pair_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, int first_flags = 0, int last_flags = 0 ) {
 			const uint64_t nc = L->num_colors;
+			if( planes_usable( L ) ) {
+				// plane.cu: even planes (colours 0-3), odd planes (4-7, 7-4), even planes (3-0); every phase out of place
+				double * const zs = L->zs->d;
+				plane_phase_enqueue( L, 0, 1, z->d, z->d, zs, zs, r, first_flags & 1 );       // z -> zs, odd planes copied along
+				plane_phase_enqueue( L, 1, 0, zs, zs, z->d, nullptr, r, 0 );                  // odd planes: zs -> z
+				plane_phase_enqueue( L, 2, 0, zs, z->d, z->d, nullptr, r, last_flags & 2 );   // even planes: zs (+ odd planes of z) -> z
+				return;
+			}
 			// small level on one process: the whole pair of sweeps in one launch (sweep_cluster.cu), same steps
 			if( L->ctx->fused_transfers && L->plan == nullptr && nc >= 1
 				&& kern::gs_sweep_cluster_usable( L->colorA, L->color_pos, L->color_size, L->n ) ) {
@@ -810,7 +846,7 @@ namespace slabgpu {
 			// launch keeps its matrix rows in registers, else they are one extra pass over the colour-0
 			// rows; the prolongation rides on the FIRST colour step of the post-smoother (forward, colour
 			// 0), which reads no other colour-0 value. Results are bit-identical to the composition above.
-			const bool fuse_residual = kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ 0 ] ) );
+			const bool fuse_residual = planes_usable( L ) || kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ 0 ] ) );
 			const bool ghosts = L->z_c->n_alloc > L->z_c->n; // distributed: the ghost tail must be zeroed too
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
 				sweep_pair_enqueue( L, z, r, 0, sweep + 1 == sweeps && fuse_residual ? 2 : 0 );

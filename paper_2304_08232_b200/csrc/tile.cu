@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -48,6 +49,7 @@ namespace slabgpu {
 			cudaFree( masks );
 		}
 		masks = nullptr;
+		regular = false;
 	}
 
 	namespace kern {
@@ -419,6 +421,34 @@ namespace slabgpu {
 				masks[ pos ] = m;
 			}
 
+			// does every row store exactly the offsets that stay inside the box? (plane.cu runs without masks then)
+			__global__ void __launch_bounds__( kBlock ) k_box_regular( const uint32_t * __restrict__ masks, const int32_t * __restrict__ rows, int64_t npos,
+				int lx, int ly, int lz, unsigned long long * bad ) {
+				const int64_t pos = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				if( pos >= npos ) {
+					return;
+				}
+				const int64_t i = rows != nullptr ? static_cast< int64_t >( rows[ pos ] ) : pos;
+				if( i < 0 ) {
+					return;
+				}
+				const int x = static_cast< int >( i % lx ), y = static_cast< int >( ( i / lx ) % ly ), zc = static_cast< int >( i / ( static_cast< int64_t >( lx ) * ly ) );
+				unsigned int m = 0u;
+				for( int dz = -1; dz <= 1; ++dz ) {
+					for( int dy = -1; dy <= 1; ++dy ) {
+						for( int dx = -1; dx <= 1; ++dx ) {
+							const int nx = x + dx, ny = y + dy, nz = zc + dz;
+							if( nx >= 0 && nx < lx && ny >= 0 && ny < ly && nz >= 0 && nz < lz ) {
+								m |= 1u << ( 9 * ( dz + 1 ) + 3 * ( dy + 1 ) + ( dx + 1 ) );
+							}
+						}
+					}
+				}
+				if( masks[ pos ] != m ) {
+					atomicAdd( bad, 1ull );
+				}
+			}
+
 			// is the colour-major row list the parity lattice the pair kernel computes positions from?
 			// position color_pos[c] + qx + sx (qy + sy qz)  <->  row (px + 2 qx) + lx ((py + 2 qy) + ly (pz + 2 qz))
 			struct LatticeParam {
@@ -678,11 +708,39 @@ namespace slabgpu {
 			throw;
 		}
 		cudaFree( d_canon );
-		cudaFree( d_bad );
 		if( bad != 0 ) {
+			cudaFree( d_bad );
 			T.release();
 			return;
 		}
+		// regular: every row stores exactly its in-box offsets, every value is finite (0 * value must be a zero)
+		bool finite = true;
+		for( int s = 0; s < 27; ++s ) {
+			finite = finite && seen[ s ] && std::isfinite( canon[ s ] );
+		}
+		T.regular = false;
+		if( finite ) {
+			unsigned long long irregular = 1;
+			cudaError_t err = cudaMemsetAsync( d_bad, 0, sizeof( unsigned long long ), st );
+			if( err == cudaSuccess ) {
+				k_box_regular<<< dev::blocks_for( std::min< int64_t >( npos, S.nrows ) ), dev::kBlock, 0, st >>>( T.masks, d_rows, std::min< int64_t >( npos, S.nrows ), lx, ly, lz, d_bad );
+				count_launch();
+				err = cudaGetLastError();
+			}
+			if( err == cudaSuccess ) {
+				err = cudaMemcpyAsync( &irregular, d_bad, sizeof( irregular ), cudaMemcpyDeviceToHost, st );
+			}
+			if( err == cudaSuccess ) {
+				err = cudaStreamSynchronize( st );
+			}
+			if( err != cudaSuccess ) {
+				cudaFree( d_bad );
+				T.release();
+				SLAB_CUDA( err );
+			}
+			T.regular = irregular == 0;
+		}
+		cudaFree( d_bad );
 		// (outside any stream capture: the launches themselves may be captured into graphs later)
 		allow_big_smem< 0 >();
 		allow_big_smem< 1 >();

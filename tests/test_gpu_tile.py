@@ -9,7 +9,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = {"tile": 1, "tile_min_rows": 200000, "tile_ty": 0, "tile_cz": 0, "tile_ns": 0}
+DEFAULTS = {"planes": 1, "tile": 1, "tile_min_rows": 200000, "tile_ty": 0, "tile_cz": 0, "tile_ns": 0}
 
 
 @pytest.fixture()
@@ -35,7 +35,7 @@ def test_sweeps_bitwise(slab, ctx, oracle, tuning, dims):
     buf, _ = oracle.random_vector(2 * n, 17)
     r, z0 = buf[:n], buf[n:]
     olvl = oracle.build_hierarchy(*dims, 1)
-    tuning(tile_min_rows=0)
+    tuning(planes=0, tile_min_rows=0)
     lvl = ctx.build_hierarchy(dims, 1)
     assert lvl.format_info()["mask_bytes"] > 0
     for name in ("rbgs_forward", "rbgs_backward", "rbgs_symmetric"):
@@ -55,7 +55,7 @@ def test_tile_shapes_bitwise(slab, ctx, oracle, tuning, shape):
     buf, _ = oracle.random_vector(2 * n, 5)
     r, z0 = buf[:n], buf[n:]
     want = oracle.rbgs_symmetric(oracle.build_hierarchy(*dims, 1), z0, r)
-    tuning(tile_min_rows=0, **shape)
+    tuning(planes=0, tile_min_rows=0, **shape)
     lvl = ctx.build_hierarchy(dims, 1)
     z = ctx.DenseVector(z0)
     slab.rbgs_symmetric(lvl, z, ctx.DenseVector(r))
@@ -70,7 +70,7 @@ def test_tile_equals_per_colour_launches_two_sweeps(slab, ctx, oracle, tuning):
     lvl = ctx.build_hierarchy(dims, 1)
     got = {}
     for rows in (0, 1 << 40):
-        tuning(tile_min_rows=rows)
+        tuning(planes=0, tile_min_rows=rows)
         z = ctx.DenseVector(z0)
         slab.rbgs_symmetric(lvl, z, ctx.DenseVector(r), slab.SmootherConfig(sweeps=2))
         got[rows] = z.values()
@@ -82,7 +82,7 @@ def test_tile_equals_per_colour_launches_two_sweeps(slab, ctx, oracle, tuning):
 def test_vcycle_with_fused_transfers_bitwise(slab, ctx, oracle, tuning):
     """prolongation on the first forward pair, residual + restriction on the last backward pair (multigrid.hpp:87-116)"""
     dims = (32, 16, 24)
-    tuning(tile_min_rows=0)
+    tuning(planes=0, tile_min_rows=0)
     h = ctx.build_hierarchy(dims, 3)
     oh = oracle.build_hierarchy(*dims, 3)
     r, _ = oracle.random_vector(h.n(), 29)
@@ -96,7 +96,7 @@ def test_solve_history_bitwise_through_tiles(slab, ctx, tuning):
     """16^3, 4 levels, exact dots: the 16^3 and 8^3 levels run the pair launches; golden history of the reference"""
     ctx.dot_mode = slab.DOT_EXACT
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "history_16.json")))
-    tuning(tile_min_rows=0)
+    tuning(planes=0, tile_min_rows=0)
     slab.set_tuning("cluster_rows", 0)
     try:
         h = ctx.build_hierarchy((16, 16, 16), 4)
