@@ -129,6 +129,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_plane_ns = static_cast< int >( value );
 		} else if( k == "plane_rows" ) {
 			g_plane_rows = static_cast< int >( value );
+		} else if( k == "plane_unit" ) {
+			g_plane_unit = value ? 1 : 0;
 		} else if( k == "persist_rows" ) {
 			g_persist_rows = value;
 		} else if( k == "halo_overlap" ) {

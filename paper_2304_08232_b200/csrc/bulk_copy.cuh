@@ -45,6 +45,23 @@ namespace slabgpu {
 					"l"( __cvta_generic_to_global( src ) ), "r"( bytes ), "r"( smem_u32( bar ) )
 					: "memory" );
 			}
+			// shared -> global bulk copy, tracked by the issuing thread's bulk async-group
+			__device__ __forceinline__ void s2g( void * dst, const void * src, unsigned int bytes ) {
+				asm volatile( "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"( __cvta_generic_to_global( dst ) ), "r"( smem_u32( src ) ),
+					"r"( bytes )
+					: "memory" );
+			}
+			__device__ __forceinline__ void commit_group() {
+				asm volatile( "cp.async.bulk.commit_group;" ::: "memory" );
+			}
+			// every committed group of this thread has finished READING its shared-memory source
+			__device__ __forceinline__ void wait_group_read0() {
+				asm volatile( "cp.async.bulk.wait_group.read 0;" ::: "memory" );
+			}
+			// every committed group of this thread is complete
+			__device__ __forceinline__ void wait_group0() {
+				asm volatile( "cp.async.bulk.wait_group 0;" ::: "memory" );
+			}
 			// generic-proxy accesses to shared memory before this point are ordered before later async-proxy ones
 			__device__ __forceinline__ void fence_proxy_async() {
 				asm volatile( "fence.proxy.async.shared::cta;" ::: "memory" );

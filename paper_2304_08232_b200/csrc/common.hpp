@@ -79,6 +79,7 @@ namespace slabgpu {
 	extern int g_use_planes;          // plane.cu: three-launch symmetric sweeps on regular box levels (default 1)
 	extern int64_t g_plane_min_rows;  // ... for levels of at least this many rows
 	extern int g_plane_ty, g_plane_cz, g_plane_ns, g_plane_rows; // shape overrides (0 = automatic)
+	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
 	}
