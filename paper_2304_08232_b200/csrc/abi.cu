@@ -119,6 +119,16 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_tile_ns = static_cast< int >( value );
 		} else if( k == "planes" ) {
 			g_use_planes = value ? 1 : 0;
+		} else if( k == "spmv_planes" ) {
+			g_use_spmv_planes = value ? 1 : 0;
+		} else if( k == "spmv_plane_min_rows" ) {
+			g_spmv_plane_min_rows = value;
+		} else if( k == "spmv_plane_ty" ) {
+			g_spmv_plane_ty = static_cast< int >( value );
+		} else if( k == "spmv_plane_cz" ) {
+			g_spmv_plane_cz = static_cast< int >( value );
+		} else if( k == "spmv_plane_ns" ) {
+			g_spmv_plane_ns = static_cast< int >( value );
 		} else if( k == "plane_min_rows" ) {
 			g_plane_min_rows = value;
 		} else if( k == "plane_ty" ) {

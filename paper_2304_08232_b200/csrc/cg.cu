@@ -69,8 +69,12 @@ namespace slabgpu {
 				// tree-dot mode: p'Ap rides on the product's epilogue and r'r on the x/r update — two
 				// passes over the vectors and two launches fewer per iteration
 				halo_exchange( H, p, -1 );
-				kern::spmv( st, H->A->sell, p->d, q->d,
-					static_cast< int64_t >( H->n ), ctx->d_partials, ctx->d_counter, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
+				if( H->A->plan == nullptr && kern::spmv_planes_usable( H->A->tile, static_cast< int64_t >( H->n ), ctx->sm_count ) ) {
+					kern::spmv_planes( st, ctx->sm_count, H->A->tile, p->d, q->d, ctx->d_partials, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
+				} else {
+					kern::spmv( st, H->A->sell, p->d, q->d,
+						static_cast< int64_t >( H->n ), ctx->d_partials, ctx->d_counter, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
+				}
 				allreduce_slot( ctx, S_PQ );
 				kern::cg_update_xr_dot( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
 					ctx->d_counter );                                                 // cg.hpp:127-132
@@ -155,7 +159,8 @@ namespace slabgpu {
 		if( graphs && limit > 0 ) {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
-				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch;
+				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
+				|| ws->key_scratch != ctx->scratch_gen;
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -205,6 +210,7 @@ namespace slabgpu {
 					ws->key_dot = ctx->dot_mode;
 					ws->key_fused = ctx->fused_transfers;
 					ws->key_epoch = g_tuning_epoch;
+					ws->key_scratch = ctx->scratch_gen;
 				}
 			}
 		}

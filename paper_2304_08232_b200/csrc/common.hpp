@@ -79,6 +79,9 @@ namespace slabgpu {
 	extern int g_use_planes;          // plane.cu: three-launch symmetric sweeps on regular box levels (default 1)
 	extern int64_t g_plane_min_rows;  // ... for levels of at least this many rows
 	extern int g_plane_ty, g_plane_cz, g_plane_ns, g_plane_rows; // shape overrides (0 = automatic)
+	extern int g_use_spmv_planes;         // plane_spmv.cu: slab-staged products of regular box matrices (default 1)
+	extern int64_t g_spmv_plane_min_rows; // ... for matrices of at least this many rows
+	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
@@ -191,6 +194,7 @@ struct slab_ctx_s {
 	double * d_scalars = nullptr;   // S_COUNT doubles
 	double * d_partials = nullptr;  // reduction scratch
 	uint64_t partials_cap = 0;
+	uint64_t scratch_gen = 0;       // bumped whenever d_partials moves: part of every cached graph's key
 	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
 	unsigned int * d_barrier = nullptr; // grid barrier of the persistent V-cycle kernel: {arrivals, generation}
 	int persist_grid = 0;               // blocks of the persistent kernel (0 = not yet sized)
@@ -268,6 +272,7 @@ struct slab_level_s {
 	uint64_t vcycle_sweeps = 0;
 	int vcycle_fused = -1;
 	uint64_t vcycle_epoch = ~uint64_t( 0 );
+	uint64_t vcycle_scratch = ~uint64_t( 0 );
 	uint64_t vcycle_launches = 0;
 	// persistent sub-V-cycle rooted at this level: device phase list, keyed by the vectors it addresses
 	void * d_phases = nullptr;
@@ -295,6 +300,7 @@ namespace slabgpu {
 		uint64_t key_sweeps = 0;
 		int key_precond = -1, key_dot = -1, key_fused = -1;
 		uint64_t key_epoch = ~uint64_t( 0 );
+		uint64_t key_scratch = ~uint64_t( 0 );
 		uint64_t iter_launches = 0;
 		~CgWorkspace();
 	};

@@ -35,6 +35,7 @@ namespace slabgpu {
 		const uint64_t cap = std::max< uint64_t >( count, 1024 );
 		SLAB_CUDA( cudaMalloc( &ctx->d_partials, cap * sizeof( double ) ) );
 		ctx->partials_cap = cap;
+		++ctx->scratch_gen; // graphs captured with the old pointer are stale (cg.cu, level.cu)
 	}
 
 	void ensure_pinned( slab_ctx_s * ctx, uint64_t doubles ) {
@@ -220,14 +221,30 @@ namespace slabgpu {
 		return A.release();
 	}
 
+	// natural-order rows as masks over the 27 offsets (tile.cu), verified against the coded copy; when the matrix
+	// turns out regular, plane_spmv.cu computes its products without a matrix stream
+	static void mat_box_tile( slab_ctx_s * ctx, slab_mat_s * A, const Decomp & D ) {
+		if( ctx->dist != nullptr || D.n_ghost != 0 || !A->sell.packed.usable() || ( D.l[ 0 ] % 2 ) != 0 || !g_use_spmv_planes ) {
+			return;
+		}
+		box_tile_build( ctx, A->sell, nullptr, D, A->tile );
+		if( A->tile.usable() && A->tile.regular ) {
+			kern::spmv_planes_prepare();
+		} else {
+			A->tile.release(); // the masks serve nothing else on a natural-order matrix
+		}
+	}
+
 	slab_mat_s * mat_stencil27( slab_ctx_s * ctx, uint64_t nx, uint64_t ny, uint64_t nz ) {
 		check_dims( nx, ny, nz );
 		std::unique_ptr< slab_mat_s > A( new slab_mat_s );
 		A->ctx = ctx;
 		A->nrows = A->ncols = nx * ny * nz;
 		A->nnz = ( 3 * nx - 2 ) * ( 3 * ny - 2 ) * ( 3 * nz - 2 ); // problem.hpp:80-82
-		A->sell = sell_stencil27( ctx, single_domain( nx, ny, nz ), nullptr, static_cast< int64_t >( A->nrows ) );
+		const Decomp D = single_domain( nx, ny, nz );
+		A->sell = sell_stencil27( ctx, D, nullptr, static_cast< int64_t >( A->nrows ) );
 		sell_pack( ctx, A->sell, nullptr );
+		mat_box_tile( ctx, A.get(), D );
 		return A.release();
 	}
 
@@ -255,6 +272,7 @@ namespace slabgpu {
 		A->nnz = nnz; // equals (3nx-2)(3ny-2)(3nz-2) on a single domain (problem.hpp:80-82)
 		A->sell = sell_stencil27( ctx, D, nullptr, static_cast< int64_t >( A->nrows ) );
 		sell_pack( ctx, A->sell, nullptr, static_cast< int64_t >( A->ncols ) ); // columns >= ncols are ghost slots
+		mat_box_tile( ctx, A.get(), D );
 		return A.release();
 	}
 
@@ -420,7 +438,9 @@ namespace slabgpu {
 		if( A->plan != nullptr && !transpose ) {
 			halo_exchange_plan( A->ctx, A->plan, x, -1 ); // ghost copies of x before the gather
 		}
-		if( mask == nullptr ) {
+		if( mask == nullptr && !transpose && kern::spmv_planes_usable( M->tile, static_cast< int64_t >( M->nrows ), A->ctx->sm_count ) ) {
+			kern::spmv_planes( st, A->ctx->sm_count, M->tile, x->d, y->d, nullptr, nullptr );
+		} else if( mask == nullptr ) {
 			kern::spmv( st, M->sell, x->d, y->d, static_cast< int64_t >( M->nrows ) );
 		} else {
 			kern::spmv_masked( st, M->sell, x->d, y->d, mask->d_members,

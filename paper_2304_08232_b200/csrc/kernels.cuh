@@ -95,6 +95,13 @@ namespace slabgpu {
 		void gs_planes( cudaStream_t st, int sm_count, const BoxTile & T, int kind, int pass, const double * own_in, const double * nb_in,
 			double * own_out, double * pass_out, const double * r, int flags, const double * src, double * out, double * zero );
 
+		// ---- plane_spmv.cu: y = A x of a regular box matrix, x staged through shared memory (every staged value read once
+		// per thread); dot_out != nullptr: x'(A x) in a fixed tree (dot_partials: spmv_planes_blocks doubles)
+		bool spmv_planes_usable( const BoxTile & T, int64_t rows, int sm_count );
+		void spmv_planes_prepare(); // function attributes; call outside stream capture
+		uint64_t spmv_planes_blocks( const BoxTile & T, int sm_count );
+		void spmv_planes( cudaStream_t st, int sm_count, const BoxTile & T, const double * x, double * y, double * dot_partials, double * dot_out );
+
 		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
 		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a
 		// kernel launch (coarse levels are launch-latency-bound). Same arithmetic, same order.

@@ -883,7 +883,7 @@ namespace slabgpu {
 			return;
 		}
 		if( L->vcycle_exec == nullptr || L->vcycle_z != z->d || L->vcycle_r != r->d || L->vcycle_sweeps != sweeps
-			|| L->vcycle_fused != ctx->fused_transfers || L->vcycle_epoch != g_tuning_epoch ) {
+			|| L->vcycle_fused != ctx->fused_transfers || L->vcycle_epoch != g_tuning_epoch || L->vcycle_scratch != ctx->scratch_gen ) {
 			if( L->vcycle_exec ) {
 				cudaGraphExecDestroy( L->vcycle_exec );
 				L->vcycle_exec = nullptr;
@@ -912,6 +912,7 @@ namespace slabgpu {
 			L->vcycle_sweeps = sweeps;
 			L->vcycle_fused = ctx->fused_transfers;
 			L->vcycle_epoch = g_tuning_epoch;
+			L->vcycle_scratch = ctx->scratch_gen;
 		}
 		SLAB_CUDA( cudaGraphLaunch( L->vcycle_exec, ctx->stream ) );
 		count_launch( L->vcycle_launches );
