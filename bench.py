@@ -101,19 +101,60 @@ def algorithmic_bytes_per_iteration(dims, levels=LEVELS):
     return total
 
 
+def sweep_bytes_model(dims):
+    """SURVEY.md §8(d) bytes of ONE symmetric sweep (16 colour steps): 2 (12 nnz + 32 n)."""
+    n = dims[0] * dims[1] * dims[2]
+    return 2 * (12 * stencil_nnz(dims) + 32 * n)
+
+
+def spmv_bytes_model(dims):
+    n = dims[0] * dims[1] * dims[2]
+    return 12 * stencil_nnz(dims) + 16 * n
+
+
 def gs_step_bytes(dims):
-    """algorithmic bytes of ONE colour-step launch on the finest level: (12 nnz + 32 n) / 8."""
+    """SURVEY model bytes of ONE colour-step launch on the finest level: (12 nnz + 32 n) / 8."""
     n = dims[0] * dims[1] * dims[2]
     return (12 * stencil_nnz(dims) + 32 * n) / 8.0
 
 
 def gs_step_bytes_coded(dims, info):
-    """bytes ONE colour-step launch has to move when the level is dictionary-coded (packed.cu): per row of the
-    colour 16 B code words x chunks + 4 B row index + r + z in + z out (8 B each), and the gathered vector once
-    per sweep (n * 8 / 8 per step) — the SURVEY model with the 12 B/nnz matrix term replaced by the codes."""
+    """bytes ONE colour-step launch has to move when the level is dictionary-coded (packed.cu; decomposed levels of the
+    multi-GPU arm): per row of the colour 16 B code words x chunks + 4 B row index + r + z in + z out (8 B each), and
+    the gathered vector once per sweep (n * 8 / 8 per step)."""
     n = dims[0] * dims[1] * dims[2]
     chunks = (info["width_class"] + 16) // 16
     return (n / 8.0) * (16 * chunks + 4 + 24) + n
+
+
+def sweep_bytes_planes(dims):
+    """bytes ONE symmetric sweep has to move in the matrix-free plane format (plane.cu, three launches): phase A
+    reads z (8n) and r on the even planes (4n) and writes every plane (8n: the even ones updated, the odd ones
+    copied along) = 20n; phases B and C each read z (8n) and r on their planes (4n) and write their planes (4n)
+    = 16n. 52 bytes per row."""
+    return 52 * dims[0] * dims[1] * dims[2]
+
+
+def spmv_bytes_planes(dims):
+    """plane_spmv.cu: x in, y out."""
+    return 16 * dims[0] * dims[1] * dims[2]
+
+
+def format_bytes_per_iteration(dims, levels=LEVELS):
+    """compulsory bytes of one CG iteration in the formats the kernels actually read: matrix-free
+    plane sweeps (52 n per symmetric sweep) and products (16 n), the fused transfers (16 n_c out, 8 n_c in), and on
+    the finest level set_all(z) 8n, r'z 16n, the p update 24n and the fused x/r update + r'r 48n."""
+    ld = level_dims(dims, levels)
+    total = 0
+    for k, d in enumerate(ld):
+        n = d[0] * d[1] * d[2]
+        last = k == len(ld) - 1 and levels > 1
+        total += (1 if last else 2) * sweep_bytes_planes(d)
+        if not last and levels > 1:
+            total += 24 * (n // 8)
+        if k == 0:
+            total += spmv_bytes_planes(d) + (8 + 16 + 24 + 48) * n
+    return total
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -217,7 +258,8 @@ def run_cpu_baseline(dims):
     return {
         "value": gflops, "unit": "GFLOP/s", "cores": o.threads, "kind": o.kind,
         "sample": f"{iters} of {CG_ITERS} CG iterations of the same {dims[0]}^3 4-level solve "
-                  f"({dt:.2f} s; hierarchy generation excluded as in bench.hpp:170-172)",
+                  f"({dt:.2f} s; hierarchy generation excluded as in bench.hpp:170-172); ONE cold run, also the parity "
+                  "check of the timed GPU solve — the number to quote is the --impl reference arm (mean of K steps after warm-up)",
     }, res
 
 
@@ -236,12 +278,13 @@ def run_reference_arm(args, dims):
     dt = time.perf_counter() - t0
     gflops = hpcg_flops_per_iteration(dims) * iters * args.steps / dt / 1e9
     sample = (f"each step = {iters} of {CG_ITERS} CG iterations of the {dims[0]}^3 4-level solve on the host cores "
-              f"(setup excluded)")
+              f"(setup excluded; a rate, so the bounded sample compares with the 50-iteration GPU step); single process "
+              f"on the grid of rank 0's local size; mean of {args.steps} steps after {args.warmup} warm-ups: the CPU number to quote")
     line = {
         "impl": "reference", "metric": "hpcg_gflops", "value": gflops, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, dims, 1, note="CPU reference arm, single process on the global grid of rank 0's local size"),
+        "config": workload_config(args.workload, dims, 1),
         "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": o.threads, "kind": o.kind, "sample": sample},
         "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -253,16 +296,16 @@ def run_reference_arm(args, dims):
 # ----------------------------------------------------------------------------- our arm
 
 
-def workload_config(name, dims, n_gpus, note=None):
+def workload_config(name, dims, n_gpus):
     grid = PROCESS_GRIDS.get(n_gpus, (n_gpus, 1, 1))
     cfg = {
         "workload": f"{name}: MG-preconditioned CG, local grid {dims[0]}x{dims[1]}x{dims[2]} per GPU, {LEVELS} MG levels, "
                     f"1 pre/1 post coloured SymGS, b=A*1, x0=0, {CG_ITERS} fixed iterations",
         "local_grid": list(dims), "process_grid": list(grid), "levels": LEVELS, "cg_iterations": CG_ITERS,
-        "l2": "per-iteration working set (matrix twice + vectors) far exceeds the 126 MB L2; no flush needed",
+        "l2": "no flush: the vectors one iteration streams through (x, r, p, q, z, its out-of-place partner, b: "
+              f"{7 * 8 * dims[0] * dims[1] * dims[2] / 1e6:.0f} MB on the finest level) exceed the 126 MB L2 at the headline "
+              "size; smaller workloads are reported as they run, L2-resident",
     }
-    if note:
-        cfg["note"] = note
     return cfg
 
 
@@ -274,15 +317,15 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def measured_traffic(dims):
-    """dram bytes per colour-step launch from the committed ncu --set full summary, if any."""
+def measured_traffic(key, dims):
+    """dram bytes per launch (read + write, live caches) from the committed ncu capture, if any: profiles/traffic.json"""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     try:
         with open(path) as fh:
             data = json.load(fh)
-        return data.get("gs_color_step", {}).get("x".join(str(d) for d in dims))
+        return data.get(key, {}).get("x".join(str(d) for d in dims))
     except (OSError, ValueError):
         return None
 
@@ -322,6 +365,70 @@ def bench_one(slab, ctx, dims, steps, warmup, dot_mode):
     flops = hpcg_flops_per_iteration(dims) * CG_ITERS * steps
     return {"h": h, "b": b, "x0": x0, "cfg": cfg, "ms": ms, "res": res, "launches": launches,
             "gflops": flops / (ms * 1e-3) / 1e9}
+
+
+def microbench_256(slab, ctx, peak):
+    """BASELINE.json configs[2]: (a) y = A x, x ~ U(-1,1) from Lcg64(0); (b) one coloured symmetric GS sweep on
+    r = b - A x from z = 0 — on the 256^3 27-point matrix, checksums compared bit for bit with the reference's
+    (tests/golden/micro_256.json, generated from the reference headers by tests/golden/make_golden.py)."""
+    dims = (256, 256, 256)
+    lvl = ctx.build_hierarchy(dims, 1)
+    n = lvl.n()
+    x, _ = ctx.random_vector(n, 0)
+    y = ctx.DenseVector(n)
+    ones = ctx.DenseVector(n, 1.0)
+    b = ctx.DenseVector(n)
+    slab.mxv(b, lvl.A, ones)
+    slab.mxv(y, lvl.A, x)
+    r = ctx.DenseVector(n)
+    slab.waxpby(r, 1.0, b, -1.0, y)
+    z = ctx.DenseVector(n, 0.0)
+    slab.rbgs_symmetric(lvl, z, r)
+    saved = ctx.dot_mode
+    ctx.dot_mode = slab.DOT_EXACT  # the reference's reduction order: the checksums compare bit for bit
+    try:
+        sums = {"dot_yy": slab.dot(y, y), "dot_xy": slab.dot(x, y), "dot_zz_after_symmetric": slab.dot(z, z),
+                "dot_rz_after_symmetric": slab.dot(r, z)}
+    finally:
+        ctx.dot_mode = saved
+    out = {"workload": "micro256: SpMV and one coloured symmetric GS sweep on the 256^3 27-point matrix (n = 16.8 M)",
+           "checksums": {k: float(v).hex() for k, v in sums.items()}}
+    gpath = os.path.join(ROOT, "tests", "golden", "micro_256.json")
+    if os.path.exists(gpath):
+        with open(gpath) as fh:
+            gold = json.load(fh)
+        out["checksums_match_reference_bitwise"] = all(sums[k] == float.fromhex(gold[k + "_hex"]) for k in sums)
+    reps = 20
+    for _ in range(3):
+        slab.mxv(y, lvl.A, x)
+    ctx.timer_start()
+    for _ in range(reps):
+        slab.mxv(y, lvl.A, x)
+    spmv_ms = ctx.timer_stop() / reps
+    slab.set_all(z, 0.0)
+    for _ in range(2):
+        slab.rbgs_symmetric(lvl, z, r)
+    launches0 = slab.launch_count()
+    ctx.timer_start()
+    for _ in range(reps):
+        slab.rbgs_symmetric(lvl, z, r)
+    gs_ms = ctx.timer_stop() / reps
+    per_sweep = (slab.launch_count() - launches0) // reps
+    info = lvl.format_info()
+    planes = bool(info.get("plane_phases")) and per_sweep == 3
+    spmv_planes = bool(lvl.A.format_info().get("plane_phases"))
+    sp_fmt = spmv_bytes_planes(dims) if spmv_planes else spmv_bytes_model(dims)
+    gs_fmt = sweep_bytes_planes(dims) if planes else sweep_bytes_model(dims)
+    out["spmv"] = {"ms": spmv_ms, "format_bytes": sp_fmt, "format_gbs": sp_fmt / spmv_ms / 1e6,
+                   "format_frac": sp_fmt / spmv_ms / 1e6 / peak, "model_frac": spmv_bytes_model(dims) / spmv_ms / 1e6 / peak,
+                   "kernel": "k_spmv_planes (plane_spmv.cu)" if spmv_planes else "row kernels"}
+    out["gs_symmetric_sweep"] = {"ms": gs_ms, "launches": per_sweep, "format_bytes": gs_fmt, "format_gbs": gs_fmt / gs_ms / 1e6,
+                                 "format_frac": gs_fmt / gs_ms / 1e6 / peak,
+                                 "model_frac": sweep_bytes_model(dims) / gs_ms / 1e6 / peak,
+                                 "kernel": "k_gs_planes x3 (plane.cu)" if planes else "per-colour steps"}
+    out["how"] = (f"CUDA events on the library stream, {reps} repetitions after warm-up, no L2 flush (a 256^3 vector is 134 MB, "
+                  "larger than the 126 MB L2); format_* = 16 B (product) / 52 B (sweep) per row, model_* = SURVEY's 12 B/nnz")
+    return out
 
 
 def main():
@@ -385,8 +492,8 @@ def main():
            "ms_per_step": e2e_ms / args.steps,
            "final_residual": eres.residual_history[-1]}
 
-    # ---- roofline of the dominant kernel: the finest-level colour step, timed alone with CUDA
-    #      events on the launching stream (16 launches per symmetric sweep)
+    # ---- roofline of the dominant kernel: the plane phases of the finest-level smoother (three launches per
+    #      symmetric sweep), timed alone with CUDA events on the launching stream
     peak, peak_src = peaks()
     roofline = None
     if not args.no_extras:
@@ -394,34 +501,41 @@ def main():
         r = main_run["b"]
         for _ in range(3):
             slab.rbgs_symmetric(h, z, r)
-        reps = 10
+        reps = 20
+        launches0 = slab.launch_count()
         ctx.timer_start()
         for _ in range(reps):
             slab.rbgs_symmetric(h, z, r)
         gs_ms = ctx.timer_stop()
-        per_launch_s = gs_ms * 1e-3 / (16 * reps)
-        achieved = gs_step_bytes(dims) / per_launch_s / 1e9
+        per_sweep = (slab.launch_count() - launches0) // reps
         info = h.format_info()
-        coded = bool(info["packed"]) and n // 8 >= 65536
-        kernel = ("k_gs_color_packed_multi<27,2,2,32>" if n // 8 >= 300000 else "k_gs_color_packed<27,2,2,32>") if coded \
-            else "k_gs_color_batched<9,5>"
-        roofline = {"bound": "hbm", "kernel": kernel + " (finest-level colour step, smoother.hpp:60-72)",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": measured_traffic(dims), "algorithmic_bytes_per_launch": gs_step_bytes(dims),
-                    "us_per_launch": per_launch_s * 1e6, "launches_per_step": 32 * CG_ITERS,
-                    "share_of_step": 32 * CG_ITERS * per_launch_s * 1e3 / ms_per_step, "peak_source": peak_src,
-                    "how": "16 launches of one symmetric sweep timed alone with CUDA events on the library stream, "
-                           "10 repetitions after 3 warm-ups; traffic = dram bytes per launch from profiles/r01_ncu_gs_packed_192.txt "
-                           "(cold cache: the gathered vector comes from DRAM there, from L2 in the live run)"}
-        if coded:
-            fb = gs_step_bytes_coded(dims, info)
-            roofline["format"] = {
-                "matrix": "dictionary-coded SELL-32 (packed.cu): 1 B per stored entry instead of the 12 B the SURVEY "
-                          "model counts, decoded exactly; frac > 1 means the launch beats the HBM time of the 12 B/nnz model",
-                "width_class": info["width_class"], "dict_size": info["dict_size"], "escaped_rows": info["escaped_rows"],
-                "bytes_per_launch": fb, "achieved": fb / per_launch_s / 1e9, "frac": fb / per_launch_s / 1e9 / peak,
-                "bound_now": "L1/L2 gather path and instruction issue (profiles/r01_ncu_gs_packed_192.txt), not HBM"}
+        planes = bool(info.get("plane_phases")) and per_sweep == 3
+        per_launch_s = gs_ms * 1e-3 / (per_sweep * reps)
+        fmt_bytes = (sweep_bytes_planes(dims) if planes else sweep_bytes_model(dims)) / per_sweep
+        model_bytes = sweep_bytes_model(dims) / per_sweep
+        achieved = fmt_bytes / per_launch_s / 1e9
+        sweeps_per_iteration = 2  # finest level: one pre-, one post-smoothing sweep
+        roofline = {
+            "bound": "hbm",
+            "kernel": ("k_gs_planes<kind,1,unit> (plane.cu: the finest level's symmetric sweep as three plane-phase launches; "
+                       "smoother.hpp:60-113)") if planes else "per-colour steps (smoother.hpp:60-72)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": measured_traffic("gs_planes_launch", dims),
+            "algorithmic_bytes_per_launch": fmt_bytes, "us_per_launch": per_launch_s * 1e6,
+            "launches_per_step": per_sweep * sweeps_per_iteration * CG_ITERS,
+            "share_of_step": per_sweep * sweeps_per_iteration * CG_ITERS * per_launch_s * 1e3 / ms_per_step,
+            "peak_source": peak_src,
+            "model_frac": model_bytes / per_launch_s / 1e9 / peak,
+            "how": f"{per_sweep} launches of one symmetric sweep timed alone with CUDA events on the library stream, {reps} "
+                   "repetitions after 3 warm-ups, averaged over the launches. achieved/frac count the bytes the matrix-free "
+                   "plane format has to move (52 B per row and sweep: z in, r in, z out; DESIGN.md §4); model_frac keeps "
+                   "SURVEY §8d's 12 B/nnz denominator (a format that streams the matrix), which this format beats by "
+                   "construction. traffic = ncu dram read+write bytes per launch with live caches (--cache-control none, "
+                   "profiles/r02_ncu_planes_192.txt). The launch is bound by the SM's shared-memory pipe, not by HBM",
+        }
 
+    flops_iter = hpcg_flops_per_iteration(dims)
+    fmt_iter = format_bytes_per_iteration(dims)
     line = {
         "metric": "hpcg_gflops", "value": main_run["gflops"], "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -429,36 +543,65 @@ def main():
         "config": workload_config(args.workload, dims, 1),
         "dot_mode": args.dot,
         "final_residual": main_run["res"].residual_history[-1],
-        "hbm_gbs_algorithmic": iter_bytes * CG_ITERS / (ms_per_step * 1e-3) / 1e9,
-        "hbm_frac_of_measured_peak": iter_bytes * CG_ITERS / (ms_per_step * 1e-3) / 1e9 / peak,
+        "hbm": {
+            "peak_gbs": peak,
+            "format_bytes_per_iteration": fmt_iter,
+            "format_gbs": fmt_iter * CG_ITERS / (ms_per_step * 1e-3) / 1e9,
+            "format_frac": fmt_iter * CG_ITERS / (ms_per_step * 1e-3) / 1e9 / peak,
+            "model_bytes_per_iteration": iter_bytes,
+            "model_frac": iter_bytes * CG_ITERS / (ms_per_step * 1e-3) / 1e9 / peak,
+            "what": "format_*: the bytes one iteration has to move in the formats the kernels read (matrix-free plane "
+                    "sweeps and products); model_*: SURVEY §8d's fused-minimum model with 12 B per stored nonzero, which "
+                    "a matrix-free format exceeds by construction (kept for comparison with matrix-streaming codes)",
+        },
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(main_run["launches"]),
     }
     if roofline:
         line["roofline"] = roofline
 
     if not args.no_extras:
-        # the same solve from the plain SELL-32 arrays (12 B per stored entry, the format SURVEY's byte model
-        # describes): what the dictionary-coded copy buys, and the number to hold against the 12 B/nnz roofline
-        slab.set_tuning("packed", 0)
+        # ---- the same solve in exact-dot mode (the reference's 4096-chunk order: histories bit-identical)
+        other_mode = slab.DOT_EXACT if args.dot == "tree" else slab.DOT_TREE
+        run = bench_one(slab, ctx, dims, 3, 3, other_mode)
+        line["exact_dots" if args.dot == "tree" else "tree_dots"] = {
+            "value": run["gflops"], "unit": "GFLOP/s", "ms_per_step": run["ms"] / 3,
+            "final_residual": run["res"].residual_history[-1]}
+        del run
+        ctx.dot_mode = dot_mode
+
+        # ---- the same solve read from the plain SELL-32 arrays (12 B per stored entry, the format SURVEY's byte
+        #      model describes): what the matrix-free kernels buy, and the number to hold against the 12 B/nnz roofline
+        plain_keys = {"packed": 0, "planes": 0, "spmv_planes": 0, "tile": 0}
+        for key, value in plain_keys.items():
+            slab.set_tuning(key, value)
         try:
             time_solves(slab, ctx, h, b, main_run["x0"], cfg, 2, ctx.DenseVector(n))
             plain_ms, _ = time_solves(slab, ctx, h, b, main_run["x0"], cfg, 3, ctx.DenseVector(n))
         finally:
-            slab.set_tuning("packed", 1)
+            for key in plain_keys:
+                slab.set_tuning(key, 1)
         plain_per = plain_ms / 3
         line["plain_sell_format"] = {"value": flops_step / (plain_per * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": plain_per,
-                                     "hbm_frac_of_measured_peak": iter_bytes * CG_ITERS / (plain_per * 1e-3) / 1e9 / peak}
+                                     "model_frac": iter_bytes * CG_ITERS / (plain_per * 1e-3) / 1e9 / peak}
         others = []
-        for name in ("hpcg104", "hpcg64"):
+        for name in ("hpcg104", "hpcg64", "hpcg16"):
             if name == args.workload:
                 continue
             d = WORKLOADS[name]
             run = bench_one(slab, ctx, d, max(args.steps, 5), 3, dot_mode)
-            ib = algorithmic_bytes_per_iteration(d)
             per = run["ms"] / max(args.steps, 5)
             others.append({"workload": name, "value": run["gflops"], "unit": "GFLOP/s", "ms_per_step": per,
-                           "hbm_frac_of_measured_peak": ib * CG_ITERS / (per * 1e-3) / 1e9 / peak})
+                           "format_frac": format_bytes_per_iteration(d) * CG_ITERS / (per * 1e-3) / 1e9 / peak,
+                           "model_frac": algorithmic_bytes_per_iteration(d) * CG_ITERS / (per * 1e-3) / 1e9 / peak})
+            del run
         line["other_workloads"] = others
+        # the 192^3 hierarchy is not needed any more: make room for the 256^3 matrices
+        del z, r
+        main_run_res = main_run["res"]
+        main_run.clear()
+        main_run["res"] = main_run_res
+        del h, b
+        line["microbench_256"] = microbench_256(slab, ctx, peak)
 
     if not args.no_cpu_baseline:
         cpu, cres = run_cpu_baseline(dims)

@@ -70,8 +70,9 @@ uint64_t slab_launch_count( void );
 int slab_set_programmatic_launch( int enabled );
 /* performance knobs that never change results: "stream_rows" (launches with at least this many rows
  * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl", "halo_overlap" (boundary
- * rows first, halo messages beside the interior rows), "persist_rows" / "persist_blocks_per_sm" (persistent
- * coarse-level kernel), "l2_window"; for the dictionary-coded matrix copy: "packed" (use it, default 1),
+ * rows first, halo messages beside the interior rows), "l2_window"; "planes" / "plane_min_rows" / "plane_ty" /
+ * "plane_cz" / "plane_ns" (plane-phase smoother of regular box levels, csrc/plane.cu) and "spmv_planes" /
+ * "spmv_plane_min_rows" / "spmv_plane_ty" / "spmv_plane_cz" / "spmv_plane_ns" (slab-staged product, csrc/plane_spmv.cu); for the dictionary-coded matrix copy: "packed" (use it, default 1),
  * "pack_build" (build it when a matrix is created, default 1), "keep_plain" (default 1; 0 frees the plain arrays of
  * matrices created afterwards whose coded copy has no escaped rows — 32 instead of 324 bytes per 27-point row, at the
  * price of download / transpose for those matrices), "packed_min_rows" (smaller launches use the plain arrays), "packed_batch", "packed_block", "packed_rows" / "packed_rows_spmv" (rows per thread of

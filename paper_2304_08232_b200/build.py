@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libslab_b200.so")
-SOURCES = ["kernels.cu", "kernels_setup.cu", "packed.cu", "tile.cu", "plane.cu", "plane_spmv.cu", "sweep_cluster.cu", "containers.cu", "level.cu", "cg.cu", "dist.cu", "abi.cu"]
+SOURCES = ["kernels.cu", "kernels_setup.cu", "packed.cu", "tile.cu", "plane.cu", "plane_spmv.cu", "sweep_cluster.cu", "coloring.cu", "containers.cu", "level.cu", "cg.cu", "dist.cu", "abi.cu"]
 HEADERS = ["common.hpp", "kernels.cuh", "device_util.cuh", "packed_decode.cuh", "bulk_copy.cuh", "decomp.hpp", "dist.hpp", os.path.join("..", "..", "include", "slab_b200.h")]
 
 NVCC_FLAGS = [

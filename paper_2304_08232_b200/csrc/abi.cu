@@ -119,6 +119,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_tile_ns = static_cast< int >( value );
 		} else if( k == "planes" ) {
 			g_use_planes = value ? 1 : 0;
+		} else if( k == "dot_cpb" ) {
+			g_dot_cpb = static_cast< int >( value );
 		} else if( k == "spmv_planes" ) {
 			g_use_spmv_planes = value ? 1 : 0;
 		} else if( k == "spmv_plane_min_rows" ) {
@@ -141,135 +143,14 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_plane_rows = static_cast< int >( value );
 		} else if( k == "plane_unit" ) {
 			g_plane_unit = value ? 1 : 0;
-		} else if( k == "persist_rows" ) {
-			g_persist_rows = value;
 		} else if( k == "halo_overlap" ) {
 			g_halo_overlap = value ? 1 : 0;
 		} else if( k == "l2_window" ) {
 			g_l2_window = static_cast< int >( value );
-		} else if( k == "persist_debug" ) {
-			g_persist_debug = static_cast< int >( value );
-		} else if( k == "persist_blocks_per_sm" ) {
-			g_persist_blocks_per_sm = static_cast< int >( value );
 		} else {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "slab_set_tuning: unknown key " + k );
 		}
 		++g_tuning_epoch;
-	} );
-}
-
-int slab_debug_read_barrier_words( slab_ctx_t ctx, long long * out6 ) {
-	return guarded( [ & ] {
-		need( ctx, "slab_debug_read_barrier_words" );
-		need( out6, "slab_debug_read_barrier_words" );
-		if( ctx->d_barrier == nullptr ) {
-			fail( SLAB_ERR_INVALID_ARGUMENT, "no persistent kernel has run on this context" );
-		}
-		SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) );
-		SLAB_CUDA( cudaMemcpy( out6, ctx->d_barrier + 40, 6 * sizeof( long long ), cudaMemcpyDeviceToHost ) );
-	} );
-}
-
-// timing experiment: one symmetric sweep with colour-major vectors; returns ms per sweep and, in
-// *max_diff, the largest |difference| to the natural-layout sweep on the same data (must be 0)
-int slab_debug_playout_sweep( slab_level_t level, slab_vec_t z, slab_vec_t r, int reps, double * ms, double * max_diff ) {
-	return guarded( [ & ] {
-		need( level, "slab_debug_playout_sweep" );
-		slab_ctx_s * ctx = level->ctx;
-		bind( ctx );
-		cudaStream_t st = ctx->stream;
-		const int64_t npos = level->color_pos[ level->num_colors ];
-		const int64_t entries = level->colorA.entries;
-		int32_t * nat2pos = nullptr;
-		int32_t * pcols = nullptr;
-		double * zp = nullptr;
-		double * rp = nullptr;
-		SLAB_CUDA( cudaMalloc( &nat2pos, level->n * sizeof( int32_t ) ) );
-		SLAB_CUDA( cudaMalloc( &pcols, entries * sizeof( int32_t ) ) );
-		SLAB_CUDA( cudaMalloc( &zp, npos * sizeof( double ) ) );
-		SLAB_CUDA( cudaMalloc( &rp, npos * sizeof( double ) ) );
-		kern::proto_invert_rows( st, level->d_rows, npos, nat2pos );
-		kern::proto_permute_cols( st, level->colorA.cols, nat2pos, entries, pcols );
-		kern::proto_gather_to_pos( st, level->d_rows, npos, z->d, zp );
-		kern::proto_gather_to_pos( st, level->d_rows, npos, r->d, rp );
-		// position-space matrix: same slices and values, permuted columns; packed against row == position.
-		// Positions of padding rows never occur as columns, but rows must not read them: the row list marks them.
-		Sell PS = level->colorA;
-		PS.cols = pcols;
-		PS.packed = Packed();
-		// one coded view per colour block: a colour's rows use at most as many pairs as a row has entries, so
-		// each view's dictionary fits the small parameter block
-		std::vector< Sell > views( level->num_colors );
-		int32_t * iota = nullptr;
-		{
-			std::vector< int32_t > h_iota( npos );
-			for( int64_t p = 0; p < npos; ++p ) h_iota[ p ] = static_cast< int32_t >( p );
-			SLAB_CUDA( cudaMalloc( &iota, std::max< int64_t >( npos, 1 ) * sizeof( int32_t ) ) );
-			upload_sync( st, iota, h_iota.data(), npos * sizeof( int32_t ) );
-		}
-		bool packed = g_use_packed != 0;
-		for( uint64_t k = 0; k < level->num_colors && packed; ++k ) {
-			Sell & V = views[ k ];
-			V = PS;
-			V.packed = Packed();
-			V.slice_off = PS.slice_off + level->color_pos[ k ] / kSlice;
-			V.nslices = ( level->color_pos[ k + 1 ] - level->color_pos[ k ] ) / kSlice;
-			V.nrows = V.nslices * kSlice;
-			sell_pack( ctx, V, iota + level->color_pos[ k ] );
-			packed = V.packed.usable();
-		}
-		const auto step = [ & ]( uint64_t k ) {
-			if( packed ) {
-				kern::gs_color_step( st, views[ k ], iota + level->color_pos[ k ], 0, static_cast< int64_t >( level->color_size[ k ] ),
-					zp, rp );
-			} else {
-				kern::proto_gs_color_pos( st, level->colorA.slice_off, level->colorA.vals, pcols, level->color_pos[ k ],
-					static_cast< int64_t >( level->color_size[ k ] ), zp, rp );
-			}
-		};
-		const auto sweep = [ & ]() {
-			for( uint64_t k = 0; k < level->num_colors; ++k ) {
-				step( k );
-			}
-			for( uint64_t k = level->num_colors; k > 0; --k ) {
-				step( k - 1 );
-			}
-		};
-		sweep(); // one sweep to compare
-		rbgs_symmetric( level, z, r, 1 );
-		std::vector< double > a( npos ), b( level->n );
-		SLAB_CUDA( cudaMemcpyAsync( a.data(), zp, npos * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
-		SLAB_CUDA( cudaMemcpyAsync( b.data(), z->d, level->n * sizeof( double ), cudaMemcpyDeviceToHost, st ) );
-		std::vector< int32_t > rows( npos );
-		SLAB_CUDA( cudaMemcpyAsync( rows.data(), level->d_rows, npos * sizeof( int32_t ), cudaMemcpyDeviceToHost, st ) );
-		SLAB_CUDA( cudaStreamSynchronize( st ) );
-		double diff = 0.0;
-		for( int64_t p = 0; p < npos; ++p ) {
-			if( rows[ p ] >= 0 ) {
-				diff = std::max( diff, std::abs( a[ p ] - b[ rows[ p ] ] ) );
-			}
-		}
-		if( max_diff ) *max_diff = diff;
-		for( int w = 0; w < 3; ++w ) sweep();
-		SLAB_CUDA( cudaEventRecord( ctx->timer_start, st ) );
-		for( int w = 0; w < reps; ++w ) sweep();
-		SLAB_CUDA( cudaEventRecord( ctx->timer_stop, st ) );
-		SLAB_CUDA( cudaEventSynchronize( ctx->timer_stop ) );
-		float t = 0.0f;
-		SLAB_CUDA( cudaEventElapsedTime( &t, ctx->timer_start, ctx->timer_stop ) );
-		if( ms ) *ms = t / reps;
-		if( packed && max_diff ) {
-			std::fprintf( stderr, "position-space dictionaries per colour: %d entries, %lld escaped rows, stride %d\n",
-				views[ 0 ].packed.dict_size, static_cast< long long >( views[ 0 ].packed.escaped_rows ), views[ 0 ].packed.stride );
-		}
-		for( Sell & V : views ) {
-			V.packed.release();
-		}
-		cudaFree( iota );
-		cudaFree( nat2pos );
-		cudaFree( pcols );
-		cudaFree( zp );
-		cudaFree( rp );
 	} );
 }
 
@@ -327,12 +208,6 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		if( const char * v = std::getenv( "SLAB_PACKED_BLOCK" ) ) {
 			g_packed_block = std::atoi( v );
 		}
-		if( const char * v = std::getenv( "SLAB_PERSIST_ROWS" ) ) {
-			g_persist_rows = std::atoll( v );
-		}
-		if( const char * v = std::getenv( "SLAB_PERSIST_BLOCKS_PER_SM" ) ) {
-			g_persist_blocks_per_sm = std::atoi( v );
-		}
 		if( const char * v = std::getenv( "SLAB_HALO_OVERLAP" ) ) {
 			g_halo_overlap = std::atoi( v ) ? 1 : 0;
 		}
@@ -356,6 +231,7 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		ctx->cc_minor = prop.minor;
 		ctx->hbm_bytes = prop.totalGlobalMem;
 		SLAB_CUDA( cudaStreamCreateWithFlags( &ctx->stream, cudaStreamNonBlocking ) );
+		kern::dot_exact_prepare();
 		SLAB_CUDA( cudaMalloc( &ctx->d_scalars, S_COUNT * sizeof( double ) ) );
 		SLAB_CUDA( cudaMemset( ctx->d_scalars, 0, S_COUNT * sizeof( double ) ) );
 		SLAB_CUDA( cudaMalloc( &ctx->d_counter, sizeof( unsigned int ) ) );
@@ -386,7 +262,6 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		cudaFree( ctx->d_scalars );
 		cudaFree( ctx->d_partials );
 		cudaFree( ctx->d_counter );
-		cudaFree( ctx->d_barrier );
 		if( ctx->h_pinned ) cudaFreeHost( ctx->h_pinned );
 		cudaEventDestroy( ctx->timer_start );
 		cudaEventDestroy( ctx->timer_stop );

@@ -53,10 +53,8 @@ namespace slabgpu {
 	}
 
 	extern uint64_t g_tuning_epoch;  // bumped by every slab_set_tuning: cached graphs are keyed by it
-	extern int64_t g_persist_rows;   // levels whose largest colour has fewer rows run inside the persistent kernel (0 = off)
-	extern int g_persist_blocks_per_sm;
-	extern int g_persist_debug;
 	extern size_t g_l2_persist_bytes;
+	extern int g_dot_cpb;             // exact dot: chunks per block override (0 = automatic)
 	extern size_t g_l2_window_max;
 	extern int g_l2_window;
 	extern int64_t g_stream_rows;
@@ -196,8 +194,6 @@ struct slab_ctx_s {
 	uint64_t partials_cap = 0;
 	uint64_t scratch_gen = 0;       // bumped whenever d_partials moves: part of every cached graph's key
 	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
-	unsigned int * d_barrier = nullptr; // grid barrier of the persistent V-cycle kernel: {arrivals, generation}
-	int persist_grid = 0;               // blocks of the persistent kernel (0 = not yet sized)
 	double * h_pinned = nullptr;    // pinned staging for scalar read-back
 	uint64_t h_pinned_cap = 0;
 	cudaEvent_t timer_start = nullptr, timer_stop = nullptr; // slab_ctx_timer_* (caller-owned interval)
@@ -274,13 +270,6 @@ struct slab_level_s {
 	uint64_t vcycle_epoch = ~uint64_t( 0 );
 	uint64_t vcycle_scratch = ~uint64_t( 0 );
 	uint64_t vcycle_launches = 0;
-	// persistent sub-V-cycle rooted at this level: device phase list, keyed by the vectors it addresses
-	void * d_phases = nullptr;
-	int nphases = 0;
-	int phases_grid = 1;
-	double * phases_z = nullptr;
-	double * phases_r = nullptr;
-	uint64_t phases_sweeps = 0;
 	// CG workspace of the hierarchy head: r, z, p, q, device history, iteration graph
 	std::unique_ptr< slabgpu::CgWorkspace > cg;
 	~slab_level_s();
@@ -332,6 +321,8 @@ namespace slabgpu {
 	// tile.cu: build T from the coded copy of S (rows: position -> natural row, nullptr = identity) on the box D;
 	// leaves T unusable when the matrix is not a subset-of-27-offsets matrix on that box
 	void box_tile_build( slab_ctx_s * ctx, const Sell & S, const int32_t * d_rows, const Decomp & D, BoxTile & T );
+	// coloring.cu: greedy_color (coloring.hpp:114-158) as a device wavefront; color[i] per row
+	void greedy_color_device( slab_ctx_s * ctx, uint64_t n, const uint64_t * ro, const uint64_t * co, std::vector< int32_t > & color, uint64_t & num_colors );
 	// is d_rows the parity lattice of the box (colour c = px + 2 py + 4 pz, members x-fastest)? The colour-pair
 	// kernel computes row positions from coordinates instead of reading the list.
 	bool box_tile_lattice_ok( slab_ctx_s * ctx, const int32_t * d_rows, const std::vector< int64_t > & color_pos, const Decomp & D );

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "common.hpp"
+#include "bulk_copy.cuh"
 #include "device_util.cuh"
 
 namespace slabgpu {
@@ -32,19 +33,13 @@ namespace slabgpu {
 	int g_use_pdl = 1;
 	// L2 persisting carve-out (set by slab_ctx_create from the device limits; 0 = unused)
 	size_t g_l2_persist_bytes = 0;
+	int g_dot_cpb = 0; // exact dot: chunks per block (0 = spread the chunks over the SMs once)
 	size_t g_l2_window_max = 0;
 	// attach an access-policy window on z to fine-level colour steps. OFF by default: measured on B200
 	// (tools/l2_window_probe.py) the carve-out helps the 192^3 sweep by 2.6% but costs 12-18% at 104^3 and
 	// 256^3, because it shrinks the L2 that everything else shares. Enable with SLAB_L2_WINDOW=1.
 	int g_l2_window = 0;
 	uint64_t g_tuning_epoch = 0;
-	// levels whose largest colour has fewer rows than this run inside the persistent V-cycle kernel.
-	// OFF by default: measured on B200 (tools/persistent_probe.py) a phase costs 3.1-4.2 us (release
-	// atomic ~0.9 us + acquire poll/fence ~1.2 us + the row's own load->gather->add chain ~1.2 us), while
-	// the same colour step as a programmatically-dependent launch inside the CUDA graph costs 1.8-2.5 us.
-	int64_t g_persist_rows = 0;
-	int g_persist_blocks_per_sm = 1;
-	int g_persist_debug = 0; // timing experiments only: 1 = barriers without work, 2 = work without grid barriers
 	// launches with at least this many rows use the streaming kernels, smaller ones the preload
 	// kernels (measured cross-over on B200: between 1.4e5 and 8.8e5 rows per launch)
 	int64_t g_stream_rows = 200000;
@@ -257,75 +252,161 @@ namespace slabgpu {
 				return acc;
 			}
 
-			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * x,
-				const double * y, uint64_t n, double * partials, unsigned int * counter, double * out ) {
-				__shared__ double prod[ 2 ][ kDotTile ];
+			// One LANE per chunk, one WARP per SM. A chain of 4096 dependent additions costs 4096 x 8.8 cycles whoever
+			// runs it, and a warp instruction with one active lane takes the FP64 pipe's issue slot like a full one — so
+			// the chunks an SM is responsible for ride in the lanes of ONE warp (lane c adds chunk c: up to 32 chains per
+			// instruction, every step at the bare latency of the addition). The operands come by the bulk-async copy
+			// engine: each lane issues the copies of its own chunk's next tiles of x and y (two contiguous pieces per
+			// tile) into a ring of stages, completion counted on the stage's mbarrier, two stages in flight while the
+			// third is consumed — bytes in flight without a register or a loader warp. Rows of a stage are `pitch`
+			// doubles apart (tile + 2: 16-byte aligned for the copies, and the lanes' reads spread over the banks). The
+			// products are rounded on their own (operations.hpp:74) sixteen ahead of the additions that consume them. The
+			// block that finishes last adds the per-chunk partials in chunk order (operations.hpp:84-90).
+			constexpr int kDotStages = 3;
+
+			// acc + x[0] y[0] + x[1] y[1] + ... left to right for ONE thread; the products of the next 16 elements are in
+			// registers before the current 16 are added (two register sets that swap roles statically)
+			__device__ __forceinline__ double chain_prod( const double * px, const double * py, int count, double acc ) {
+				constexpr int kStep = 16;
+				double ra[ kStep ], rb[ kStep ];
+				#pragma unroll
+				for( int k = 0; k < kStep; ++k ) {
+					ra[ k ] = k < count ? __dmul_rn( px[ k ], py[ k ] ) : 0.0;
+				}
+				int i = 0;
+				for( ; i + 2 * kStep <= count; i += 2 * kStep ) {
+					#pragma unroll
+					for( int k = 0; k < kStep; ++k ) {
+						rb[ k ] = __dmul_rn( px[ i + kStep + k ], py[ i + kStep + k ] );
+					}
+					#pragma unroll
+					for( int k = 0; k < kStep; ++k ) {
+						acc = __dadd_rn( acc, ra[ k ] );
+					}
+					#pragma unroll
+					for( int k = 0; k < kStep; ++k ) {
+						ra[ k ] = i + 2 * kStep + k < count ? __dmul_rn( px[ i + 2 * kStep + k ], py[ i + 2 * kStep + k ] ) : 0.0;
+					}
+					#pragma unroll
+					for( int k = 0; k < kStep; ++k ) {
+						acc = __dadd_rn( acc, rb[ k ] );
+					}
+				}
+				#pragma unroll
+				for( int k = 0; k < kStep; ++k ) {
+					if( i + k < count ) {
+						acc = __dadd_rn( acc, ra[ k ] );
+					}
+				}
+				for( int j = i + kStep; j < count; ++j ) {
+					acc = __dadd_rn( acc, __dmul_rn( px[ j ], py[ j ] ) );
+				}
+				return acc;
+			}
+
+			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * x, const double * y, uint64_t n, int cpb, int tile, double * partials,
+				unsigned int * counter, double * out ) {
+				extern __shared__ __align__( 128 ) unsigned char dot_smem[];
+				uint64_t * const full = reinterpret_cast< uint64_t * >( dot_smem );
+				double * const stage0 = reinterpret_cast< double * >( dot_smem + 128 ); // [kDotStages][2][cpb][pitch]
+				const int lane = threadIdx.x;
+				const int pitch = tile + 2;
+				const size_t stage_elems = static_cast< size_t >( 2 ) * cpb * pitch;
+				if( lane == 0 ) {
+					for( int s = 0; s < kDotStages; ++s ) {
+						bulk::mbar_init( full + s, 1u );
+					}
+					bulk::mbar_fence_init();
+				}
+				__syncwarp();
 				dep_trigger();
 				dep_wait();
-				const uint64_t begin = static_cast< uint64_t >( blockIdx.x ) * kDotChunk;
-				const uint64_t remaining = n - begin;
-				const int len = static_cast< int >( remaining < kDotChunk ? remaining : kDotChunk );
-				const int lane = threadIdx.x;
-				const int ntiles = ( len + kDotTile - 1 ) / kDotTile;
-				constexpr int kPer = kDotTile / 32; // products per lane and tile
-				double a[ kPer ], c[ kPer ];
-				const auto tile_load = [ & ]( int t ) { // coalesced: lane l takes elements l, l + 32, ... of the tile
+				const uint64_t nchunks = ( n + kDotChunk - 1 ) / kDotChunk;
+				const uint64_t chunk0 = static_cast< uint64_t >( blockIdx.x ) * cpb;
+				const int nmine = static_cast< int >( nchunks - chunk0 < static_cast< uint64_t >( cpb ) ? nchunks - chunk0 : cpb );
+				const int ntiles = static_cast< int >( kDotChunk ) / tile;
+				const uint64_t begin = ( chunk0 + lane ) * kDotChunk; // this lane's chunk
+				const int len = lane < nmine ? static_cast< int >( n - begin < kDotChunk ? n - begin : kDotChunk ) : 0;
+				const bool aligned = ( ( reinterpret_cast< uintptr_t >( x ) | reinterpret_cast< uintptr_t >( y ) ) & 15 ) == 0;
+				// tile t of every chunk of the block into stage t % kDotStages: whole, 16-byte-aligned pieces by bulk copies,
+				// a ragged or unaligned piece by the lane itself (+0.0 behind the end of the vector: adding a +0.0 product to
+				// a sum that started from +0.0 changes nothing)
+				const auto issue = [ & ]( int t ) {
+					const int s = t % kDotStages;
+					double * const xs = stage0 + s * stage_elems + static_cast< size_t >( lane ) * pitch;
+					double * const ys = xs + static_cast< size_t >( cpb ) * pitch;
+					const int have = len - t * tile < 0 ? 0 : ( len - t * tile < tile ? len - t * tile : tile );
+					const bool by_copy = aligned && have == tile;
+					unsigned int bytes = by_copy ? static_cast< unsigned int >( tile ) * 16u : 0u;
 					#pragma unroll
-					for( int k = 0; k < kPer; ++k ) {
-						const int i = t * kDotTile + k * 32 + lane;
-						a[ k ] = i < len ? x[ begin + i ] : 0.0;
-						c[ k ] = i < len ? y[ begin + i ] : 0.0;
+					for( int o = 16; o > 0; o >>= 1 ) {
+						bytes += __shfl_xor_sync( 0xffffffffu, bytes, o );
 					}
-				};
-				const auto tile_store = [ & ]( int t ) {
-					#pragma unroll
-					for( int k = 0; k < kPer; ++k ) {
-						prod[ t & 1 ][ k * 32 + lane ] = __dmul_rn( a[ k ], c[ k ] );
-					}
-				};
-				tile_load( 0 );
-				tile_store( 0 );
-				__syncwarp();
-				double acc = 0.0;
-				for( int t = 0; t < ntiles; ++t ) {
-					if( t + 1 < ntiles ) {
-						tile_load( t + 1 ); // in flight while the chain below runs
-					}
-					const int count = len - t * kDotTile < kDotTile ? len - t * kDotTile : kDotTile;
-					if( lane == 0 ) {
-						acc = chain_sum( prod[ t & 1 ], count, acc );
-					}
-					if( t + 1 < ntiles ) {
-						tile_store( t + 1 );
+					if( lane < nmine && !by_copy ) {
+						for( int i = 0; i < tile; ++i ) {
+							xs[ i ] = i < have ? x[ begin + static_cast< uint64_t >( t ) * tile + i ] : 0.0;
+							ys[ i ] = i < have ? y[ begin + static_cast< uint64_t >( t ) * tile + i ] : 0.0;
+						}
 					}
 					__syncwarp();
+					if( lane == 0 ) {
+						if( bytes > 0u ) {
+							bulk::mbar_arrive_expect_tx( full + s, bytes );
+						} else {
+							bulk::mbar_arrive( full + s );
+						}
+					}
+					__syncwarp();
+					if( by_copy ) {
+						bulk::g2s( xs, x + begin + static_cast< uint64_t >( t ) * tile, static_cast< unsigned int >( tile ) * 8u, full + s );
+						bulk::g2s( ys, y + begin + static_cast< uint64_t >( t ) * tile, static_cast< unsigned int >( tile ) * 8u, full + s );
+					}
+				};
+				for( int t = 0; t < kDotStages - 1 && t < ntiles; ++t ) {
+					issue( t );
 				}
+				double acc = 0.0;
+				#pragma unroll 1
+				for( int t = 0; t < ntiles; ++t ) {
+					if( t + kDotStages - 1 < ntiles ) {
+						issue( t + kDotStages - 1 ); // into the stage consumed in the previous round
+					}
+					const int s = t % kDotStages;
+					bulk::mbar_wait( full + s, static_cast< unsigned int >( ( t / kDotStages ) & 1 ) );
+					if( lane < nmine ) {
+						const double * const xs = stage0 + s * stage_elems + static_cast< size_t >( lane ) * pitch;
+						acc = chain_prod( xs, xs + static_cast< size_t >( cpb ) * pitch, tile, acc );
+					}
+					__syncwarp();
+					bulk::fence_proxy_async(); // the stage is read; the copy engine may write it again
+				}
+				if( lane < nmine ) {
+					partials[ chunk0 + lane ] = acc;
+				}
+				__threadfence();
+				__syncwarp();
 				unsigned int ticket = 0u;
 				if( lane == 0 ) {
-					partials[ blockIdx.x ] = acc;
-					__threadfence();
 					ticket = atomicAdd( counter, 1u );
 				}
 				ticket = __shfl_sync( 0xffffffffu, ticket, 0 );
 				if( ticket != gridDim.x - 1 ) {
 					return;
 				}
-				// the warp that finishes last adds the per-chunk partials in chunk order: again a chain for lane 0,
-				// fed through shared memory in tiles that all lanes fetch together (one L2 round trip per tile, not
-				// one per group of loads of a single thread)
+				// the warp that finishes last adds the per-chunk partials in chunk order: a chain for lane 0, fed through
+				// shared memory in tiles that all lanes fetch together
 				__threadfence();
-				const int count = static_cast< int >( gridDim.x );
+				const int room = static_cast< int >( kDotStages * stage_elems < 2048 ? kDotStages * stage_elems : 2048 );
 				double total = 0.0;
-				for( int t0 = 0; t0 < count; t0 += 2 * kDotTile ) {
-					double * buf = &prod[ 0 ][ 0 ]; // both tiles as one buffer of 1024
-					const int m = count - t0 < 2 * kDotTile ? count - t0 : 2 * kDotTile;
+				for( uint64_t t0 = 0; t0 < nchunks; t0 += room ) {
+					const int m = static_cast< int >( nchunks - t0 < static_cast< uint64_t >( room ) ? nchunks - t0 : room );
 					__syncwarp();
 					for( int i = lane; i < m; i += 32 ) {
-						buf[ i ] = __ldcg( partials + t0 + i );
+						stage0[ i ] = __ldcg( partials + t0 + i );
 					}
 					__syncwarp();
 					if( lane == 0 ) {
-						total = chain_sum( buf, m, total );
+						total = chain_sum( stage0, m, total );
 					}
 				}
 				if( lane == 0 ) {
@@ -669,190 +750,6 @@ namespace slabgpu {
 				}
 			}
 
-			// ---- persistent sub-V-cycle (coarse levels): phases separated by a grid barrier
-
-			// sense-reversing grid barrier; bar[0] = arrival counter, bar[1] = generation. All blocks are
-			// co-resident (cooperative launch). Writes before the barrier are visible device-wide after
-			// it (thread 0 fences on both sides, the block barriers extend that to the whole block).
-			__device__ __forceinline__ unsigned int atom_add_release( unsigned int * p, unsigned int v ) {
-				unsigned int old;
-				asm volatile( "atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"( old ) : "l"( p ), "r"( v ) : "memory" );
-				return old;
-			}
-			__device__ __forceinline__ unsigned int load_acquire( const unsigned int * p ) {
-				unsigned int v;
-				asm volatile( "ld.acquire.gpu.global.u32 %0, [%1];" : "=r"( v ) : "l"( p ) : "memory" );
-				return v;
-			}
-			__device__ __forceinline__ void store_release( unsigned int * p, unsigned int v ) {
-				asm volatile( "st.release.gpu.global.u32 [%0], %1;" ::"l"( p ), "r"( v ) : "memory" );
-			}
-
-			// Split grid barrier. `generation` is thread 0's running copy of bar[32] (barriers are strictly
-			// sequential, so it never has to be re-read). arrive: one release-atomic by thread 0, cumulative
-			// over the block's writes through the preceding block barrier. Between arrive and wait the block
-			// may issue loads of IMMUTABLE data (the next phase's matrix rows) — issued after the release they
-			// are not ordered before it and overlap the barrier latency. wait: acquire poll plus a gpu-scope
-			// fence, which invalidates the SM's L1 so that later plain loads see the other SMs' writes.
-			__device__ __forceinline__ void grid_arrive( unsigned int * bar, unsigned int nblocks, unsigned int & generation,
-				bool & last ) {
-				__syncthreads();
-				if( threadIdx.x == 0 ) {
-					last = atom_add_release( bar, 1u ) == nblocks - 1;
-					generation += 1u;
-				}
-			}
-			__device__ __forceinline__ void grid_wait( unsigned int * bar, unsigned int generation, bool last ) {
-				if( threadIdx.x == 0 ) {
-					unsigned int * gen = bar + 32; // a different 128 B line than the arrival counter
-					if( last ) {
-						bar[ 0 ] = 0u;
-						store_release( gen, generation );
-					} else {
-						while( load_acquire( gen ) != generation ) {
-							__nanosleep( 20 );
-						}
-					}
-					__threadfence();
-				}
-				__syncthreads();
-			}
-
-			constexpr int kMaxPhases = 192; // phase descriptors staged in shared memory
-
-			// One colour-step row of the persistent kernel. `rc` holds the row's matrix entries (loaded
-			// before the preceding grid barrier); all 27 gathers go out together. Plain (L1-cached)
-			// loads are correct here: the grid barrier ends with a gpu-scope fence by thread 0 followed by
-			// a block barrier, which orders every later load of the block after the other SMs' released
-			// writes (the fence invalidates the SM's L1), exactly like cooperative-groups grid.sync().
-			//  PROLONG (flags & 1): z[i] <- 1*z[i] + 1*(0 + 1*src[k]) first (multigrid.hpp:71-81 at the injected
-			//    row); the updated value also replaces the stale diagonal gather.
-			//  RESID (flags & 2): after the update, r_c[k] = 0 + 1*(1*r[i] + (-1)*(A z)[i]) with the NEW z[i] on
-			//    the diagonal (multigrid.hpp:100-104): all other colours are final in the last backward step.
-			__device__ __forceinline__ void persistent_row( const VcyclePhase & ph, int64_t k, int32_t i, const RowChunk & rc ) {
-				double xv[ kChunk ];
-				#pragma unroll
-				for( int j = 0; j < kChunk; ++j ) {
-					xv[ j ] = ph.z[ rc.c[ j ] < 0 ? 0 : rc.c[ j ] ]; // slots beyond the width carry column -1
-				}
-				const bool prolong = ( ph.flags & 1 ) != 0;
-				double zi = ph.z[ i ];
-				const double ri = ph.r[ i ];
-				if( prolong ) {
-					const double f = __dadd_rn( 0.0, __dmul_rn( 1.0, ph.src[ k ] ) );
-					zi = __dadd_rn( __dmul_rn( 1.0, zi ), __dmul_rn( 1.0, f ) );
-				}
-				double s = 0.0, d = 0.0;
-				#pragma unroll
-				for( int j = 0; j < kChunk; ++j ) {
-					const bool diagonal = rc.c[ j ] == i;
-					const double xj = ( prolong && diagonal ) ? zi : xv[ j ];
-					const double sum = __dadd_rn( s, __dmul_rn( rc.v[ j ], xj ) );
-					s = rc.c[ j ] < 0 ? s : sum;
-					d = diagonal ? rc.v[ j ] : d;
-				}
-				const double znew = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
-				ph.z[ i ] = znew;
-				if( ph.flags & 2 ) {
-					double az = 0.0;
-					#pragma unroll
-					for( int j = 0; j < kChunk; ++j ) {
-						const double xj = rc.c[ j ] == i ? znew : xv[ j ];
-						const double sum = __dadd_rn( az, __dmul_rn( rc.v[ j ], xj ) );
-						az = rc.c[ j ] < 0 ? az : sum;
-					}
-					const double f = __dadd_rn( __dmul_rn( 1.0, ri ), __dmul_rn( -1.0, az ) );
-					ph.out[ k ] = __dadd_rn( 0.0, __dmul_rn( 1.0, f ) );
-				}
-			}
-
-			__device__ __forceinline__ void persistent_load( const VcyclePhase & ph, int64_t k, int32_t & i, RowChunk & rc,
-				int & width ) {
-				const int64_t pos = ph.pos_begin + k;
-				i = ph.rows[ pos ];
-				const int64_t s = pos >> 5;
-				const int64_t b = ph.slice_off[ s ];
-				width = static_cast< int >( ( ph.slice_off[ s + 1 ] - b ) >> 5 );
-				chunk_load( ph.vals, ph.cols, b + ( pos & 31 ), width, rc );
-			}
-
-			// One block per SM, all co-resident (cooperative launch). Every phase is one colour step of one
-			// level (smoother.hpp:60-72) with the grid transfers fused into the neighbouring colour-0 steps.
-			// A thread owns row k = its global index of every phase; the matrix entries of its NEXT row
-			// are fetched before the grid barrier, so after the barrier only the z gathers (L2 latency), the
-			// ordered add chain and one store separate two barriers.
-			__global__ void __launch_bounds__( kBlock, 1 ) k_vcycle_persistent( const VcyclePhase * __restrict__ phases,
-				int nphases, unsigned int * bar, int debug ) {
-				__shared__ VcyclePhase sph[ kMaxPhases ];
-				for( int t = threadIdx.x; t < nphases * static_cast< int >( sizeof( VcyclePhase ) / 8 ); t += blockDim.x ) {
-					reinterpret_cast< uint64_t * >( sph )[ t ] = reinterpret_cast< const uint64_t * >( phases )[ t ];
-				}
-				__syncthreads();
-				const int64_t gtid = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				const int64_t gsize = static_cast< int64_t >( gridDim.x ) * blockDim.x;
-				RowChunk rc;
-				int32_t row = -1;
-				int width = 0;
-				unsigned int generation = threadIdx.x == 0 ? *reinterpret_cast< volatile unsigned int * >( bar + 32 ) : 0u;
-				if( gtid < sph[ 0 ].count ) {
-					persistent_load( sph[ 0 ], gtid, row, rc, width );
-				}
-				long long t_work = 0, t_rest = 0, t_arrive = 0, t_pref = 0, t_wait = 0;
-				for( int p = 0; p < nphases; ++p ) {
-					const VcyclePhase & ph = sph[ p ];
-					const long long c0 = clock64();
-					if( gtid < ph.count && row >= 0 && debug != 1 ) {
-						persistent_row( ph, gtid, row, rc );
-					}
-					const long long c1 = clock64();
-					for( int64_t k = gtid + gsize; k < ph.count; k += gsize ) { // phases larger than the grid
-						RowChunk extra;
-						int32_t i;
-						int w;
-						persistent_load( ph, k, i, extra, w );
-						if( i >= 0 ) {
-							persistent_row( ph, k, i, extra );
-						}
-					}
-					for( int64_t k = gtid; k < ph.zero_count; k += gsize ) { // set_all(z_c, 0), multigrid.hpp:104
-						ph.zero[ k ] = 0.0;
-					}
-					const long long c2 = clock64();
-					if( p + 1 < nphases ) {
-						bool last = false;
-						if( debug != 2 ) {
-							grid_arrive( bar, gridDim.x, generation, last );
-						}
-						const long long c3 = clock64();
-						row = -1;
-						if( gtid < sph[ p + 1 ].count ) {
-							persistent_load( sph[ p + 1 ], gtid, row, rc, width ); // immutable data, overlaps the barrier
-						}
-						const long long c4 = clock64();
-						if( debug != 2 ) {
-							grid_wait( bar, generation, last );
-						} else {
-							__syncthreads();
-						}
-						const long long c5 = clock64();
-						t_work += c1 - c0;
-						t_rest += c2 - c1;
-						t_arrive += c3 - c2;
-						t_pref += c4 - c3;
-						t_wait += c5 - c4;
-					}
-				}
-				if( debug == 3 && gtid == 0 ) {
-					long long * out = reinterpret_cast< long long * >( bar + 40 );
-					out[ 0 ] = t_work;
-					out[ 1 ] = t_rest;
-					out[ 2 ] = t_arrive;
-					out[ 3 ] = t_pref;
-					out[ 4 ] = t_wait;
-					out[ 5 ] = nphases;
-				}
-			}
-
 			// ---- streaming forms (many-wave launches on the fine level); same arithmetic, same order
 
 			__global__ void __launch_bounds__( kBlock ) k_residual_restrict_stream( const int64_t * __restrict__ slice_off,
@@ -984,62 +881,7 @@ namespace slabgpu {
 				*iter_counter = it + 1;
 			}
 
-			// ---- prototype: colour-major ("P") vector layout. Vector entry of row position p lives at p.
-			__global__ void k_permute_cols( const int32_t * __restrict__ cols, const int32_t * __restrict__ nat2pos,
-				int64_t entries, int32_t * out ) {
-				const int64_t e = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( e < entries ) {
-					const int32_t c = cols[ e ];
-					out[ e ] = c < 0 ? -1 : nat2pos[ c ];
-				}
-			}
-			__global__ void k_invert_rows( const int32_t * __restrict__ rows, int64_t npos, int32_t * __restrict__ nat2pos ) {
-				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( p < npos && rows[ p ] >= 0 ) {
-					nat2pos[ rows[ p ] ] = static_cast< int32_t >( p );
-				}
-			}
-			__global__ void k_gather_to_pos( const int32_t * __restrict__ rows, int64_t npos, const double * __restrict__ nat,
-				double * pos ) {
-				const int64_t p = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( p < npos ) {
-					pos[ p ] = rows[ p ] >= 0 ? nat[ rows[ p ] ] : 0.0;
-				}
-			}
-			template< int B, int MINBLOCKS >
-			__global__ void __launch_bounds__( kBlock, MINBLOCKS ) k_gs_color_pos( const int64_t * __restrict__ slice_off,
-				const double * __restrict__ vals, const int32_t * __restrict__ pcols, int64_t pos_begin, int64_t pos_count,
-				double * z, const double * r ) {
-				dep_trigger();
-				dep_wait();
-				const int64_t k = static_cast< int64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
-				if( k >= pos_count ) {
-					return;
-				}
-				const int64_t pos = pos_begin + k;
-				double d = 0.0;
-				const double s = row_sum_batched< B, true >( slice_off, vals, pcols, pos, z, static_cast< int32_t >( pos ), d );
-				const double zi = z[ pos ];
-				const double ri = r[ pos ];
-				z[ pos ] = __ddiv_rn( __dadd_rn( __dadd_rn( ri, -s ), __dmul_rn( zi, d ) ), d );
-			}
-
 		} // namespace
-
-		// prototype entry points (tools/playout_probe.py)
-		void proto_permute_cols( cudaStream_t st, const int32_t * cols, const int32_t * nat2pos, int64_t entries, int32_t * out ) {
-			k_permute_cols<<< blocks_for( entries ), kBlock, 0, st >>>( cols, nat2pos, entries, out );
-		}
-		void proto_invert_rows( cudaStream_t st, const int32_t * rows, int64_t npos, int32_t * nat2pos ) {
-			k_invert_rows<<< blocks_for( npos ), kBlock, 0, st >>>( rows, npos, nat2pos );
-		}
-		void proto_gather_to_pos( cudaStream_t st, const int32_t * rows, int64_t npos, const double * nat, double * pos ) {
-			k_gather_to_pos<<< blocks_for( npos ), kBlock, 0, st >>>( rows, npos, nat, pos );
-		}
-		void proto_gs_color_pos( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * pcols,
-			int64_t pos_begin, int64_t pos_count, double * z, const double * r ) {
-			launch( k_gs_color_pos< 9, 5 >, blocks_for( pos_count ), kBlock, st, slice_off, vals, pcols, pos_begin, pos_count, z, r );
-		}
 
 		// ================================================================ wrappers
 
@@ -1075,14 +917,61 @@ namespace slabgpu {
 			launch( k_waxpby, vector_grid( n ), kBlock, st, w, alpha, x, beta, y, n );
 		}
 
+		namespace {
+			// products per chunk and stage: as long as three stages of every chunk of the block fit shared memory
+			int dot_exact_tile( int cpb ) {
+				return cpb <= 14 ? 256 : ( cpb <= 28 ? 128 : 64 );
+			}
+			size_t dot_exact_smem( int cpb, int tile ) {
+				return 128 + static_cast< size_t >( kDotStages ) * 2 * cpb * ( tile + 2 ) * sizeof( double );
+			}
+		} // namespace
+
+		void dot_exact_prepare() { // function attributes; outside any stream capture
+			static bool done = false;
+			if( !done ) {
+				SLAB_CUDA( cudaFuncSetAttribute( k_dot_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( 200 * 1024 ) ) );
+				done = true;
+			}
+		}
+
 		void dot_exact( cudaStream_t st, const double * x, const double * y, uint64_t n, double * partials,
 			unsigned int * counter, double * out ) {
 			if( n == 0 ) {
 				launch( k_dot_empty, 1, 1, st, out );
 				return;
 			}
-			const unsigned int nchunks = static_cast< unsigned int >( ( n + kDotChunk - 1 ) / kDotChunk );
-			launch( k_dot_exact, nchunks, 32, st, x, y, n, partials, counter, out );
+			// as many chunks per block as spread the chunks over the SMs once (at most one per lane of the adding warp)
+			const uint64_t nchunks = ( n + kDotChunk - 1 ) / kDotChunk;
+			static int sms = 0;
+			if( sms == 0 ) {
+				int device = 0;
+				SLAB_CUDA( cudaGetDevice( &device ) );
+				SLAB_CUDA( cudaDeviceGetAttribute( &sms, cudaDevAttrMultiProcessorCount, device ) );
+			}
+			int cpb = static_cast< int >( ( nchunks + sms - 1 ) / sms );
+			cpb = cpb < 1 ? 1 : ( cpb > 32 ? 32 : cpb );
+			if( g_dot_cpb > 0 ) {
+				cpb = g_dot_cpb > 32 ? 32 : g_dot_cpb;
+			}
+			const unsigned int grid = static_cast< unsigned int >( ( nchunks + cpb - 1 ) / cpb );
+			const int tile = dot_exact_tile( cpb );
+			cudaLaunchConfig_t cfg{};
+			cfg.gridDim = dim3( grid, 1, 1 );
+			cfg.blockDim = dim3( 32, 1, 1 );
+			cfg.dynamicSmemBytes = dot_exact_smem( cpb, tile );
+			cfg.stream = st;
+			cudaLaunchAttribute attr[ 1 ];
+			unsigned int count = 0;
+			if( g_use_pdl ) {
+				attr[ count ].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+				attr[ count ].val.programmaticStreamSerializationAllowed = 1;
+				++count;
+			}
+			cfg.attrs = attr;
+			cfg.numAttrs = count;
+			SLAB_CUDA( cudaLaunchKernelEx( &cfg, k_dot_exact, x, y, n, cpb, tile, partials, counter, out ) );
+			count_launch();
 		}
 
 		uint64_t dot_tree_blocks( uint64_t n, int sm_count ) {
@@ -1260,35 +1149,6 @@ namespace slabgpu {
 				return;
 			}
 			launch( k_prolong_add, blocks_for( n_coarse ), kBlock, st, rows, n_coarse, z, z_c );
-		}
-
-		int vcycle_persistent_blocks( int sm_count, int blocks_per_sm ) {
-			int resident = 0;
-			SLAB_CUDA( cudaOccupancyMaxActiveBlocksPerMultiprocessor( &resident, k_vcycle_persistent, kBlock, 0 ) );
-			if( resident < 1 ) {
-				fail( SLAB_ERR_CUDA, "persistent V-cycle kernel cannot be resident" );
-			}
-			const int per_sm = blocks_per_sm < resident ? blocks_per_sm : resident;
-			return sm_count * ( per_sm < 1 ? 1 : per_sm );
-		}
-
-		void vcycle_persistent( cudaStream_t st, const VcyclePhase * d_phases, int nphases, unsigned int * d_barrier,
-			int grid_blocks ) {
-			if( nphases == 0 ) {
-				return;
-			}
-			cudaLaunchConfig_t cfg{};
-			cfg.gridDim = dim3( static_cast< unsigned int >( grid_blocks ), 1, 1 );
-			cfg.blockDim = dim3( kBlock, 1, 1 );
-			cfg.dynamicSmemBytes = 0;
-			cfg.stream = st;
-			cudaLaunchAttribute attr[ 1 ];
-			attr[ 0 ].id = cudaLaunchAttributeCooperative; // all blocks co-resident: the grid barrier is safe
-			attr[ 0 ].val.cooperative = 1;
-			cfg.attrs = attr;
-			cfg.numAttrs = 1;
-			SLAB_CUDA( cudaLaunchKernelEx( &cfg, k_vcycle_persistent, d_phases, nphases, d_barrier, g_persist_debug ) );
-			count_launch();
 		}
 
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,

@@ -19,6 +19,7 @@ namespace slabgpu {
 		void waxpby( cudaStream_t st, double * w, double alpha, const double * x, double beta, const double * y,
 			uint64_t n );
 		// dot, exact: 4096-chunk ordered (operations.hpp:61-91). partials needs ceil(n/4096) doubles.
+		void dot_exact_prepare(); // function attributes; call outside stream capture
 		void dot_exact( cudaStream_t st, const double * x, const double * y, uint64_t n, double * partials,
 			unsigned int * counter, double * out );
 		// dot, fixed-shape tree. partials needs dot_tree_blocks(n, sms) doubles.
@@ -101,36 +102,6 @@ namespace slabgpu {
 		void spmv_planes_prepare(); // function attributes; call outside stream capture
 		uint64_t spmv_planes_blocks( const BoxTile & T, int sm_count );
 		void spmv_planes( cudaStream_t st, int sm_count, const BoxTile & T, const double * x, double * y, double * dot_partials, double * dot_out );
-
-		// ---- persistent sub-V-cycle: every colour step / transfer of the levels below a size threshold
-		// runs as a *phase* of ONE cooperative kernel, phases separated by a grid barrier instead of a
-		// kernel launch (coarse levels are launch-latency-bound). Same arithmetic, same order.
-		struct VcyclePhase { // one colour step; 8-byte fields only (staged into shared memory word by word)
-			int64_t flags; // bit 0: prolongation fused in front (src), bit 1: residual+restriction fused behind (out)
-			const int64_t * slice_off;
-			const double * vals;
-			const int32_t * cols;
-			const int32_t * rows;
-			int64_t pos_begin;
-			int64_t count;
-			double * z;
-			const double * r;
-			const double * src; // flags&1: the coarse correction z_c, indexed by coarse row
-			double * out;       // flags&2: r_c
-			double * zero;      // flags&2: z_c, zeroed for the coarser level's start (multigrid.hpp:104)
-			int64_t zero_count;
-		};
-		constexpr int kVcycleMaxPhases = 192;
-		int vcycle_persistent_blocks( int sm_count, int blocks_per_sm );
-		void vcycle_persistent( cudaStream_t st, const VcyclePhase * d_phases, int nphases, unsigned int * d_barrier,
-			int grid_blocks );
-
-		// ---- prototype of the colour-major vector layout (timing experiments only)
-		void proto_permute_cols( cudaStream_t st, const int32_t * cols, const int32_t * nat2pos, int64_t entries, int32_t * out );
-		void proto_invert_rows( cudaStream_t st, const int32_t * rows, int64_t npos, int32_t * nat2pos );
-		void proto_gather_to_pos( cudaStream_t st, const int32_t * rows, int64_t npos, const double * nat, double * pos );
-		void proto_gs_color_pos( cudaStream_t st, const int64_t * slice_off, const double * vals, const int32_t * pcols,
-			int64_t pos_begin, int64_t pos_count, double * z, const double * r );
 
 		// ---- CG vector updates with device-resident scalars (cg.hpp:116-132)
 		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)

@@ -17,9 +17,6 @@ slab_level_s::~slab_level_s() {
 		cudaGraphExecDestroy( vcycle_exec );
 	}
 	slabgpu::halo_plan_destroy( plan );
-	if( d_phases ) {
-		cudaFree( d_phases );
-	}
 }
 
 namespace slabgpu {
@@ -249,10 +246,9 @@ namespace slabgpu {
 		return head.release();
 	}
 
-	// ProblemLevel(SparseMatrix) problem.hpp:253 for an arbitrary square system. Setup runs on the
-	// host exactly like the reference's: extract_diagonal (problem.hpp:143-166) and greedy_color
-	// (coloring.hpp:114-158) over pattern(A) united with pattern(A^T), rows in increasing order,
-	// smallest colour not used by an already coloured neighbour.
+	// ProblemLevel(SparseMatrix) problem.hpp:253 for an arbitrary square system: extract_diagonal
+	// (problem.hpp:143-166) over the host CSR the caller handed in, greedy_color (coloring.hpp:114-158) on the
+	// device (coloring.cu), the rows of a colour in ascending order (coloring.hpp:148-151).
 	slab_level_s * level_from_csr( slab_ctx_s * ctx, uint64_t n, const uint64_t * ro, const uint64_t * co,
 		const double * va ) {
 		std::unique_ptr< slab_level_s > L( new slab_level_s );
@@ -275,46 +271,11 @@ namespace slabgpu {
 			diag[ i ] = va[ hit - co ];
 		}
 
-		// adjacency of the transpose pattern, so that non-symmetric patterns colour like the reference
-		std::vector< uint64_t > t_off( n + 1, 0 );
-		for( uint64_t k = 0; k < L->nnz; ++k ) {
-			++t_off[ co[ k ] + 1 ];
-		}
-		for( uint64_t i = 0; i < n; ++i ) {
-			t_off[ i + 1 ] += t_off[ i ];
-		}
-		std::vector< uint64_t > t_idx( L->nnz ), cursor( t_off.begin(), t_off.end() - 1 );
-		for( uint64_t i = 0; i < n; ++i ) {
-			for( uint64_t k = ro[ i ]; k < ro[ i + 1 ]; ++k ) {
-				t_idx[ cursor[ co[ k ] ]++ ] = i;
-			}
-		}
-		constexpr uint64_t unset = std::numeric_limits< uint64_t >::max();
-		std::vector< uint64_t > color( n, unset );
-		std::vector< uint64_t > stamp; // stamp[c] == i  <=>  colour c is taken around row i
+		// greedy_color on the device (coloring.cu): colour(i) = smallest colour no lower-index neighbour of
+		// pattern(A) united with pattern(A^T) has — the sequential result, evaluated as a wavefront
+		std::vector< int32_t > color;
 		uint64_t num_colors = 0;
-		for( uint64_t i = 0; i < n; ++i ) {
-			const auto forbid = [ & ]( uint64_t j ) {
-				if( j != i && color[ j ] != unset ) {
-					if( color[ j ] >= stamp.size() ) {
-						stamp.resize( color[ j ] + 1, unset );
-					}
-					stamp[ color[ j ] ] = i;
-				}
-			};
-			for( uint64_t k = ro[ i ]; k < ro[ i + 1 ]; ++k ) {
-				forbid( co[ k ] );
-			}
-			for( uint64_t k = t_off[ i ]; k < t_off[ i + 1 ]; ++k ) {
-				forbid( t_idx[ k ] );
-			}
-			uint64_t pick = 0;
-			while( pick < stamp.size() && stamp[ pick ] == i ) {
-				++pick;
-			}
-			color[ i ] = pick;
-			num_colors = std::max( num_colors, pick + 1 );
-		}
+		greedy_color_device( ctx, n, ro, co, color, num_colors );
 
 		L->num_colors = num_colors;
 		L->color_size.assign( num_colors, 0 );
@@ -614,137 +575,6 @@ namespace slabgpu {
 		}
 	} // namespace
 
-	namespace {
-
-		// A level runs inside the persistent kernel when its colour steps are latency-bound (few rows),
-		// the fused transfers are on, and no halo exchange sits between its phases.
-		uint64_t persistent_phase_count( const slab_level_s * L, uint64_t sweeps );
-
-		bool use_persistent( const slab_level_s * L, uint64_t sweeps ) {
-			if( g_persist_rows <= 0 || !L->ctx->fused_transfers || L->num_colors == 0 ) {
-				return false;
-			}
-			if( L->plan != nullptr && L->decomp.n_ghost > 0 ) {
-				return false;
-			}
-			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
-				if( at->plan != nullptr && at->decomp.n_ghost > 0 ) {
-					return false;
-				}
-			}
-			if( !L->is_stencil ) {
-				return false; // the fused transfers rely on "colour 0 == injected rows" and rows of <= 27 entries
-			}
-			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
-				if( at->colorA.plain_dropped() ) {
-					return false; // the persistent kernel reads the plain arrays
-				}
-			}
-			uint64_t largest = 0;
-			for( const uint64_t size : L->color_size ) {
-				largest = std::max( largest, size );
-			}
-			return static_cast< int64_t >( largest ) < g_persist_rows
-				&& persistent_phase_count( L, sweeps ) <= static_cast< uint64_t >( kern::kVcycleMaxPhases );
-		}
-
-		uint64_t persistent_phase_count( const slab_level_s * L, uint64_t sweeps ) {
-			uint64_t count = 0;
-			for( const slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
-				count += ( at->coarser ? 2 : 1 ) * 2 * sweeps * at->num_colors;
-			}
-			return count;
-		}
-
-		// multigrid.hpp:87-116 unrolled into the phase list of the sub-hierarchy rooted at L
-		void build_phases( slab_level_s * L, double * z, const double * r, uint64_t sweeps,
-			std::vector< kern::VcyclePhase > & out ) {
-			// On a stencil level the injected rows are exactly colour 0, in coarse-index order
-			// (position p of the colour-0 block <-> coarse row p). So the residual+restriction rides on
-			// the LAST colour step of the pre-smoother (backward, colour 0: every other colour is final
-			// by then) and the prolongation+update on the FIRST colour step of the post-smoother
-			// (forward, colour 0, which reads no other colour-0 value).
-			const auto color_step = [ & ]( uint64_t k, int64_t flags ) {
-				kern::VcyclePhase ph{};
-				ph.flags = flags;
-				ph.slice_off = L->colorA.slice_off;
-				ph.vals = L->colorA.vals;
-				ph.cols = L->colorA.cols;
-				ph.rows = L->d_rows;
-				ph.pos_begin = L->color_pos[ k ];
-				ph.count = static_cast< int64_t >( L->color_size[ k ] );
-				ph.z = z;
-				ph.r = r;
-				if( flags & 1 ) {
-					ph.src = L->z_c->d;
-				}
-				if( flags & 2 ) {
-					ph.out = L->r_c->d;
-					ph.zero = L->z_c->d;
-					ph.zero_count = static_cast< int64_t >( L->z_c->n_alloc );
-				}
-				out.push_back( ph );
-			};
-			const bool transfers = L->coarser != nullptr;
-			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) { // pre-smooth, multigrid.hpp:94
-				for( uint64_t k = 0; k < L->num_colors; ++k ) {
-					color_step( k, 0 );
-				}
-				for( uint64_t k = L->num_colors; k > 0; --k ) {
-					color_step( k - 1, transfers && sweep + 1 == sweeps && k == 1 ? 2 : 0 );
-				}
-			}
-			if( !transfers ) {
-				return;
-			}
-			build_phases( L->coarser.get(), L->z_c->d, L->r_c->d, sweeps, out );
-			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) { // post-smooth, multigrid.hpp:111
-				for( uint64_t k = 0; k < L->num_colors; ++k ) {
-					color_step( k, sweep == 0 && k == 0 ? 1 : 0 );
-				}
-				for( uint64_t k = L->num_colors; k > 0; --k ) {
-					color_step( k - 1, 0 );
-				}
-			}
-		}
-
-		void prepare_persistent( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
-			slab_ctx_s * ctx = L->ctx;
-			if( ctx->d_barrier == nullptr ) {
-				SLAB_CUDA( cudaMalloc( &ctx->d_barrier, 128 * sizeof( unsigned int ) ) );
-				const unsigned int zeros[ 128 ] = { 0u };
-				upload_sync( ctx->stream, ctx->d_barrier, zeros, sizeof( zeros ) );
-			}
-			if( ctx->persist_grid == 0 ) {
-				ctx->persist_grid = kern::vcycle_persistent_blocks( ctx->sm_count, g_persist_blocks_per_sm );
-			}
-			if( L->d_phases != nullptr && L->phases_z == z->d && L->phases_r == r->d && L->phases_sweeps == sweeps ) {
-				return;
-			}
-			std::vector< kern::VcyclePhase > phases;
-			build_phases( L, z->d, r->d, sweeps, phases );
-			SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) ); // nobody may still be reading the old list
-			if( L->d_phases != nullptr ) {
-				cudaFree( L->d_phases );
-				L->d_phases = nullptr;
-			}
-			SLAB_CUDA( cudaMalloc( &L->d_phases, std::max< size_t >( phases.size(), 1 ) * sizeof( kern::VcyclePhase ) ) );
-			upload_sync( ctx->stream, L->d_phases, phases.data(), phases.size() * sizeof( kern::VcyclePhase ) );
-			L->nphases = static_cast< int >( phases.size() );
-			// as few blocks as the widest phase needs (one row per thread): the grid barrier gets cheaper
-			// with every block that does not take part
-			int64_t widest = 1;
-			for( const kern::VcyclePhase & ph : phases ) {
-				widest = std::max( widest, ph.count );
-			}
-			L->phases_grid = static_cast< int >( std::min< int64_t >( ctx->persist_grid, ( widest + 255 ) / 256 ) );
-			L->phases_z = z->d;
-			L->phases_r = r->d;
-			L->phases_sweeps = sweeps;
-		}
-
-	} // namespace
-
 	void mg_vcycle_prepare( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) {
 		slab_ctx_s * ctx = L->ctx;
 		if( !ctx->fused_transfers ) {
@@ -752,14 +582,9 @@ namespace slabgpu {
 				mat_transposed( at->R.get() ); // built lazily; allocation is illegal during capture
 			}
 		}
-		for( slab_level_s * at = L; at != nullptr; at = at->coarser.get() ) {
-			if( use_persistent( at, sweeps ) ) {
-				prepare_persistent( at, z, r, sweeps );
-				return;
-			}
-			z = at->z_c.get();
-			r = at->r_c.get();
-		}
+		(void) z;
+		(void) r;
+		(void) sweeps;
 	}
 
 	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
@@ -807,17 +632,6 @@ namespace slabgpu {
 			}
 			if( count_stats ) {
 				L->stats.nnz_visited += L->coarser ? 4 * sweeps * L->nnz + L->nnz + 2 * L->R->nnz : 2 * sweeps * L->nnz;
-			}
-			return;
-		}
-		if( use_persistent( L, sweeps ) ) {
-			if( L->d_phases == nullptr || L->phases_z != z->d || L->phases_r != r->d || L->phases_sweeps != sweeps ) {
-				fail( SLAB_ERR_INTERNAL, "persistent V-cycle used without mg_vcycle_prepare" );
-			}
-			kern::vcycle_persistent( ctx->stream, static_cast< const kern::VcyclePhase * >( L->d_phases ), L->nphases,
-				ctx->d_barrier, L->phases_grid );
-			if( count_stats ) {
-				vcycle_stats( L, sweeps );
 			}
 			return;
 		}

@@ -13,25 +13,18 @@
 // free and the iterates are bit-identical (tests/test_gpu_cluster_sweep.py). The grid transfers ride on the
 // first and last step exactly as they do there (flags bit 0 / bit 1).
 //
-// Two modes, chosen by the level's largest colour (tuning key "cluster_rows", default 384):
-//  * one CTA (up to 512 rows per colour, one row per thread), __syncthreads between the colours. ON by default for
-//    colours of at most 384 rows: 16^3 4-level solve 10.6 -> 7.0 ms, 32^3 11.9 -> 9.7 ms, 64^3 14.3 -> 13.5 ms,
-//    104^3 20.2 -> 19.8 ms (tools/solve_sweep.py). The dictionary is copied to shared memory here, one 16-byte
-//    read per entry: the rows of a small level are all boundary rows, a warp's codes differ, and constant loads
-//    with a different index per lane are replayed per distinct index (dictionary in the constant bank: 7.9 /
-//    10.3 / 13.7 ms; in shared memory as two reads per entry and z unswizzled: 7.5 / 10.0 / 13.6 ms). One SM
-//    does the whole level, so at 512 rows per colour the mode only breaks even (64^3: 14.2 ms).
-//  * one thread-block cluster (up to 16 CTAs): every CTA holds a full copy of z, gathers from its own copy and
-//    stores a row's new value into every copy through distributed shared memory; the cluster barrier separates
-//    the colours. Correct, but no gain — measured with z in global memory first (2.1-2.6 us per phase; 64^3 14.08
-//    -> 13.84 ms, 192^3 57.0 -> 58.8 ms), then as described (104^3 20.2 -> 23.1 ms, 192^3 56.9 -> 58.2 ms for
-//    their 26^3 / 24^3 levels). The SASS says why: `barrier.cluster.arrive.release` — also what cooperative
-//    groups' cluster.sync() emits — is MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR in front of UCGABAR_ARV, and
-//    `wait.acquire` adds CCTL.IVALL: a device-wide memory barrier per phase wherever the data lives (the ncu
-//    source page has the stall on exactly those instructions). It costs what a kernel boundary costs, so the
-//    2.2 us "launch floor" of a colour step is really the price of publishing one colour's values. The way
-//    past it: `arrive.relaxed` for the write-after-read edge only, the values themselves sent
-//    with st.async + mbarrier complete_tx. Reached only when "cluster_rows" is raised above 512.
+// One CTA (up to 512 rows per colour, one row per thread), __syncthreads between the colours; ON by default for
+// levels whose largest colour has at most 384 rows (tuning key "cluster_rows") and that the plane phases of plane.cu
+// do not serve (odd or tiny boxes, general matrices): 16^3 4-level solve 10.6 -> 7.0 ms when it was introduced. The
+// dictionary is copied to shared memory here, one 16-byte read per entry: the rows of a small level are all boundary
+// rows, a warp's codes differ, and constant loads with a different index per lane are replayed per distinct index.
+//
+// A second mode — one thread-block cluster of up to 16 CTAs, z replicated in every CTA and updated through distributed
+// shared memory — was built, measured and REMOVED in round 2: bit-identical but slower than the per-colour launches
+// (104^3 20.2 -> 23.1 ms), because `barrier.cluster.arrive.release` (also what cooperative groups' cluster.sync()
+// emits) is MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR in front of UCGABAR_ARV and `wait.acquire` adds CCTL.IVALL: a
+// device-wide memory barrier per colour, i.e. what a kernel boundary costs. The levels it was meant for now run the
+// three-launch plane phases (plane.cu). The template parameter SINGLE below is what is left of it.
 #include "kernels.cuh"
 
 #include <algorithm>
@@ -46,8 +39,8 @@
 
 namespace slabgpu {
 
-	// largest colour (rows) of a level that takes the one-launch sweep: up to 512 one CTA, above that (at most 4096)
-	// a cluster; 0 = per-colour launches everywhere. Default: the range where the one-CTA mode wins (see above).
+	// largest colour (rows) of a level that takes the one-launch sweep (one CTA: at most 512); 0 = per-colour
+	// launches everywhere
 	int64_t g_cluster_rows = 384;
 
 	namespace kern {
@@ -321,7 +314,6 @@ namespace slabgpu {
 				unsigned int ctas, unsigned int block, size_t smem, double * z, const double * r, int first_flags, int last_flags,
 				const double * src, double * out, double * zero ) {
 				constexpr int C = ( N + 16 ) / 16;
-				constexpr int W = ( N + 3 ) / 4; // every gather of the row in flight at once: the phase is latency-bound
 				if( ctas == 1 ) {
 					auto kernel = k_gs_sweep_cluster< N, C, 2, D, true >; // 512 threads: the two-word batches' register count
 					static bool prepared = false;
@@ -333,15 +325,9 @@ namespace slabgpu {
 						last_flags, src, out, zero );
 					return;
 				}
-				auto kernel = k_gs_sweep_cluster< N, C, W, D, false >;
-				static bool large_clusters_allowed = false; // clusters of more than 8 CTAs are opt-in per kernel
-				if( !large_clusters_allowed ) {
-					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1 ) );
-					SLAB_CUDA( cudaFuncSetAttribute( kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( kMaxSweepSmem ) ) );
-					large_clusters_allowed = true;
-				}
-				launch_cluster( kernel, ctas, block, smem, st, P.codes, dict_param< D >( P ), plain, rows, sc, z, r, first_flags, last_flags,
-					src, out, zero );
+				// the multi-CTA cluster form (z replicated per CTA, updates through distributed shared memory) was measured
+				// and lost to the per-colour launches (file header): it is not instantiated any more
+				fail( SLAB_ERR_INTERNAL, "gs_sweep_cluster: the level does not fit one CTA" );
 			}
 
 			template< int D >
@@ -370,7 +356,7 @@ namespace slabgpu {
 				return false;
 			}
 			const uint64_t largest = *std::max_element( color_size.begin(), color_size.end() );
-			const int64_t limit = std::min< int64_t >( g_cluster_rows, static_cast< int64_t >( kMaxClusterCtas ) * kBlock );
+			const int64_t limit = std::min< int64_t >( g_cluster_rows, static_cast< int64_t >( kSingleBlock ) ); // one CTA, one row per thread
 			if( largest < 1 || static_cast< int64_t >( largest ) > limit || color_pos[ nc - 1 ] >= ( int64_t( 1 ) << 30 ) ) {
 				return false;
 			}

@@ -1,6 +1,6 @@
 """Generates the golden fixtures in tests/golden/ from the UNMODIFIED reference headers.
 
-Run in the build container (where /root/reference exists):  python tests/golden/make_golden.py [--big]
+Run in the build container (where /root/reference exists):  python tests/golden/make_golden.py [--big] [--scale]
 It loads oracle/_ref/libslab_ref.so (oracle/ref_shim.cpp compiled against
 /root/reference/proj/include by oracle/Makefile) and records
 
@@ -9,6 +9,8 @@ It loads oracle/_ref/libslab_ref.so (oracle/ref_shim.cpp compiled against
   small_cases.json     seeded small-case vectors: SpMV, masked/transposed mxv, dot, waxpby,
                        forward/backward/symmetric smoothing, a 2-level V-cycle, LCG outputs
   micro_256.json       (--big) the 256^3 microbench checksums of BASELINE.md §4
+  history_208x104x104.json, history_208x208x104.json, history_208x208x208.json
+                       (--scale) histories on the global grids of the 2-, 4- and 8-rank 104^3-per-GPU runs
 
 Nothing on the GPU box reads /root/reference: the tests read these JSON files only.
 Doubles are stored as hex strings (float.hex) so that the fixtures are bit-exact.
@@ -38,7 +40,8 @@ def dump(name, obj):
 
 
 def history(ref, n, levels=4, iters=50):
-    h = ref.build_hierarchy(n, n, n, levels)
+    dims = (n, n, n) if isinstance(n, int) else tuple(n)
+    h = ref.build_hierarchy(*dims, levels)
     b = ref.level_mxv(h, np.ones(h.n))
     res = ref.cg_solve(h, b, np.zeros(h.n), max_iters=iters, fixed_iterations=iters)
     stats = []
@@ -48,7 +51,7 @@ def history(ref, n, levels=4, iters=50):
         lvl = lvl.coarser
     return {
         "source": "reference headers via oracle/_ref (cg.hpp:77-142)",
-        "dims": [n, n, n], "levels": levels, "rhs": "A*ones", "x0": "zeros",
+        "dims": list(dims), "levels": levels, "rhs": "A*ones", "x0": "zeros",
         "iterations": res.iterations,
         "residual_history": res.residual_history,
         "residual_history_hex": hexlist(res.residual_history),
@@ -151,3 +154,8 @@ if __name__ == "__main__":
     if "--big" in sys.argv:
         dump("history_104.json", history(ref, 104))
         dump("micro_256.json", micro_256(ref))
+    if "--scale" in sys.argv:
+        # the GLOBAL grids of the weak-scaled 104^3-per-GPU runs (BASELINE.json configs[3]: process grids 2x1x1, 2x2x1,
+        # 2x2x2): the oracle of an N-rank solve is the single-process solve on the global grid
+        for dims in ((208, 104, 104), (208, 208, 104), (208, 208, 208)):
+            dump("history_%dx%dx%d.json" % dims, history(ref, dims))

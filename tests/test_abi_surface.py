@@ -97,3 +97,9 @@ def test_bench_counting_matches_survey_denominators():
     n, nnz = 256 ** 3, 766 ** 3
     assert 8 * bench.gs_step_bytes((256, 256, 256)) * 2 == 2 * (12 * nnz + 32 * n)  # 11.861 GB per symmetric sweep
     assert np.isclose(2 * (12 * nnz + 32 * n), 11.861e9, rtol=1e-3)
+    assert bench.sweep_bytes_model((256, 256, 256)) == 2 * (12 * nnz + 32 * n)
+    assert bench.spmv_bytes_model((256, 256, 256)) == 12 * nnz + 16 * n  # 5.662 GB
+    # the matrix-free plane format: 52 B per row and symmetric sweep, 16 B per row and product
+    assert bench.sweep_bytes_planes((192, 192, 192)) == 52 * 192 ** 3
+    assert bench.spmv_bytes_planes((256, 256, 256)) == 16 * n
+    assert bench.format_bytes_per_iteration((192, 192, 192)) < bench.algorithmic_bytes_per_iteration((192, 192, 192)) / 8

@@ -1,6 +1,7 @@
-"""The one-launch sweep (csrc/sweep_cluster.cu, tuning key cluster_rows: one CTA up to 512 rows per colour — the
-default for small levels — and a thread-block cluster above) must give the bits of the per-colour launches and of
-the oracle: smoother.hpp:103-113, multigrid.hpp:87-116."""
+"""The one-launch sweep (csrc/sweep_cluster.cu, tuning key cluster_rows: one CTA, up to 512 rows per colour; levels
+with larger colours keep their other kernels whatever the key says) must give the bits of the per-colour launches
+and of the oracle: smoother.hpp:103-113, multigrid.hpp:87-116. The plane phases are switched off here so that the
+even boxes reach this kernel too."""
 import json
 import os
 
@@ -17,13 +18,15 @@ def cluster_rows():
     def apply(rows):
         _capi.set_tuning("cluster_rows", rows)
 
+    _capi.set_tuning("planes", 0)
     yield apply
     apply(384)  # the library default
+    _capi.set_tuning("planes", 1)
 
 
 @pytest.mark.parametrize("dims", [(8, 8, 8), (16, 16, 16), (5, 7, 9), (26, 26, 26), (32, 32, 32), (3, 3, 3)])
 def test_symmetric_sweep_bitwise(slab, ctx, oracle, cluster_rows, dims):
-    """even, odd (unequal colour sizes) and the largest eligible grid (4096 rows per colour, 16 CTAs)"""
+    """even, odd (unequal colour sizes), the largest eligible grid (16^3: 512 rows per colour) and two that are too large"""
     n = dims[0] * dims[1] * dims[2]
     buf, _ = oracle.random_vector(2 * n, 11)
     r, z0 = buf[:n], buf[n:]

@@ -284,6 +284,70 @@ def test_general_level_coloring_matches_oracle_greedy(slab, ctx, oracle):
         slab.ProblemLevel(ctx, ([0, 1, 2], [1, 0], [1.0, 1.0]))
 
 
+def _csr_of(dense):
+    n = dense.shape[0]
+    ro = np.zeros(n + 1, dtype=np.uint64)
+    co, va = [], []
+    for i in range(n):
+        nz = np.nonzero(dense[i])[0]
+        co.extend(nz)
+        va.extend(dense[i, nz])
+        ro[i + 1] = len(co)
+    return ro, np.array(co, dtype=np.uint64), np.array(va, dtype=np.float64)
+
+
+def _same_coloring(lvl, olvl):
+    assert lvl.num_colors == olvl.num_colors
+    for k in range(lvl.num_colors):
+        assert np.array_equal(lvl.color_members(k), olvl.color_members(k))
+        assert lvl.color_info(k)[1] == olvl.color_nnz(k)
+
+
+def test_device_greedy_coloring_is_the_sequential_greedy(slab, ctx, oracle):
+    """greedy_color as a device wavefront (coloring.cu) against the oracle's sequential loop (coloring.hpp:114-158):
+    a tridiagonal chain (every row waits for the one before: as many rounds as rows, several ticketed blocks), the
+    random symmetric matrices of tests/oracles.hpp:233-272, a strictly lower-triangular pattern (the neighbours come
+    from A^T only), the 5x7x9 stencil handed in as a general matrix (eight parity classes), and a dense block whose
+    rows need more than 256 colours (the search beyond the bit mask)."""
+    n = 1500
+    tri = np.zeros((n, n))
+    idx = np.arange(n)
+    tri[idx, idx] = 2.0
+    tri[idx[1:], idx[:-1]] = -1.0
+    tri[idx[:-1], idx[1:]] = -1.0
+    ro, co, va = _csr_of(tri)
+    lvl = slab.ProblemLevel(ctx, (ro, co, va))
+    _same_coloring(lvl, oracle.level_from_csr(ro, co, va))
+    assert lvl.num_colors == 2
+    rng = np.random.default_rng(5)
+    for n, density in ((40, 0.2), (300, 0.03), (700, 0.01)):
+        m = (rng.random((n, n)) < density).astype(float)
+        m = -(m + m.T > 0).astype(float)
+        np.fill_diagonal(m, n)
+        ro, co, va = _csr_of(m)
+        _same_coloring(slab.ProblemLevel(ctx, (ro, co, va)), oracle.level_from_csr(ro, co, va))
+    low = np.tril((rng.random((200, 200)) < 0.05).astype(float) * -1.0, -1)
+    np.fill_diagonal(low, 4.0)
+    ro, co, va = _csr_of(low)
+    _same_coloring(slab.ProblemLevel(ctx, (ro, co, va)), oracle.level_from_csr(ro, co, va))
+    ro, co, va = oracle.build_matrix(5, 7, 9)
+    lvl = slab.ProblemLevel(ctx, (ro, co, va))
+    olvl = oracle.level_from_csr(ro, co, va)
+    _same_coloring(lvl, olvl)
+    assert lvl.num_colors == 8
+    for k in range(8):
+        want = [ix + 5 * (iy + 7 * iz) for iz in range(9) for iy in range(7) for ix in range(5)
+                if (ix % 2) + 2 * (iy % 2) + 4 * (iz % 2) == k]
+        assert list(lvl.color_members(k)) == want
+    n = 300
+    full = -np.ones((n, n))
+    np.fill_diagonal(full, float(n))
+    ro, co, va = _csr_of(full)
+    lvl = slab.ProblemLevel(ctx, (ro, co, va))
+    _same_coloring(lvl, oracle.level_from_csr(ro, co, va))
+    assert lvl.num_colors == n
+
+
 # ------------------------------------------------------------------ smoother.hpp
 
 

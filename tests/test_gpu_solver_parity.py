@@ -82,6 +82,31 @@ def test_full_size_104_history_matches_reference_golden(slab, ctx):
     ctx.dot_mode = slab.DOT_EXACT
 
 
+@pytest.mark.parametrize("dims", [(208, 104, 104), (208, 208, 104), (208, 208, 208)])
+def test_global_grids_of_the_weak_scaled_runs_match_reference_golden(slab, ctx, dims):
+    """The oracle of an N-rank run is the single-process solve on the GLOBAL grid: the reference's
+    histories on the global grids of the 2-, 4- and 8-rank 104^3-per-GPU runs (BASELINE.json configs[3]; fixtures from
+    tests/golden/make_golden.py --scale) — here against the single-GPU solve on the same grids, bit for bit in
+    exact-dot mode, 1e-10 in tree-dot mode. distributed_bench.py holds the N-rank histories against the same files."""
+    gold = _golden("history_%dx%dx%d.json" % dims)
+    h = ctx.build_hierarchy(dims, 4)
+    b = _rhs_A_ones(slab, ctx, h)
+    x0 = ctx.DenseVector(h.n(), 0.0)
+    cfg = slab.CGConfig(max_iters=50, fixed_iterations=50)
+    ctx.dot_mode = slab.DOT_EXACT
+    res = slab.cg_solve(h, b, x0, cfg)
+    assert res.iterations == 50
+    assert [float(v).hex() for v in res.residual_history] == gold["residual_history_hex"]
+    assert slab.dot(res.solution, res.solution) == float.fromhex(gold["solution_checksum_dot_xx_hex"])
+    ctx.dot_mode = slab.DOT_TREE
+    try:
+        tree = slab.cg_solve(h, b, x0, cfg)
+    finally:
+        ctx.dot_mode = slab.DOT_EXACT
+    want = np.array(gold["residual_history"])
+    assert np.max(np.abs(np.array(tree.residual_history) - want) / want) <= 1e-10
+
+
 def test_full_size_192_history_matches_reference_samples(slab, ctx):
     """BASELINE.json configs[4] at its real size (192^3 per GPU): the reference's residual norms recorded in
     BASELINE.md §4 (printed with 17 significant digits from the reference headers on the CPU) at iterations

@@ -46,6 +46,26 @@ def test_residual_history_equals_reference_golden(oracle, n):
     assert visited == [s["nnz_visited"] for s in g["levels_stats"]]
 
 
+def test_scale_fixtures_first_iterations_equal_port():
+    """tests/golden/history_208x104x104.json (the global grid of the 2-rank 104^3-per-GPU run, generated from the
+    reference headers by make_golden.py --scale): the port reproduces its first norms bit for bit (six iterations keep
+    the CPU tier short; CG is deterministic, so the first k+1 norms of a k-iteration run are those of the 50-iteration
+    one). The three fixtures carry 51 norms each and the decimal values below."""
+    from oracle.oracle import Oracle
+
+    o = Oracle("port")
+    g = load("history_208x104x104.json")
+    assert g["dims"] == [208, 104, 104] and g["iterations"] == 50 and len(g["residual_history_hex"]) == 51
+    h = o.build_hierarchy(208, 104, 104, 4)
+    b = o.level_mxv(h, np.ones(h.n))
+    res = o.cg_solve(h, b, np.zeros(h.n), max_iters=6, fixed_iterations=6)
+    assert np.array_equal(np.array(res.residual_history), unhex(g["residual_history_hex"][:7]))
+    assert g["residual_history"][0] == 2977.4526024774937 and g["residual_history"][50] == 0.40229533813705876
+    g4, g8 = load("history_208x208x104.json"), load("history_208x208x208.json")
+    assert g4["residual_history"][0] == 3761.3837879163566 and g4["residual_history"][50] == 1.8799785740272754
+    assert g8["residual_history"][0] == 4602.497582834781 and g8["residual_history"][50] == 8.733140867113194
+
+
 def test_baseline_md_decimal_values():
     """The decimal table of BASELINE.md §4 and the hex fixtures are the same numbers."""
     g16, g64 = load("history_16.json"), load("history_64.json")
