@@ -50,7 +50,10 @@ namespace slabgpu {
 		}
 
 		// one CG iteration, cg.hpp:110-132, enqueue only
-		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg ) {
+		// deferred (fixed-iteration solves on a communicator): r'r of an iteration is not reduced where it is computed
+		// but travels with the next iteration's r'z in one allreduce of two doubles — one collective less per iteration,
+		// no change to any rank's arithmetic; the history entry of iteration k-1 is written inside iteration k
+		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred ) {
 			slab_ctx_s * ctx = H->ctx;
 			cudaStream_t st = ctx->stream;
 			slab_vec_s * r = ws->r.get();
@@ -63,8 +66,14 @@ namespace slabgpu {
 			} else {
 				op_waxpby( z, 1.0, r, 0.0, r ); // cg.hpp:114
 			}
-			op_dot_to_slot( r, z, S_RHO );                                        // cg.hpp:116
+			op_dot_to_slot( r, z, S_RHO, !deferred );                             // cg.hpp:116
+			if( deferred ) {
+				allreduce_slots( ctx, S_RHO, 2 ); // r'z of this iteration, r'r of the one before (0 in front of the first)
+			}
 			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
+			if( deferred ) {
+				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, false );
+			}
 			if( ctx->dot_mode == SLAB_DOT_TREE ) {
 				// tree-dot mode: p'Ap rides on the product's epilogue and r'r on the x/r update — two
 				// passes over the vectors and two launches fewer per iteration
@@ -78,14 +87,18 @@ namespace slabgpu {
 				allreduce_slot( ctx, S_PQ );
 				kern::cg_update_xr_dot( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
 					ctx->d_counter );                                                 // cg.hpp:127-132
-				allreduce_slot( ctx, S_RR );
+				if( !deferred ) {
+					allreduce_slot( ctx, S_RR );
+				}
 			} else {
 				op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
 				op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
 				kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
-				op_dot_to_slot( r, r, S_RR );                                         // cg.hpp:132
+				op_dot_to_slot( r, r, S_RR, !deferred );                              // cg.hpp:132
 			}
-			kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
+			if( !deferred ) {
+				kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
+			}
 		}
 
 		void vcycle_stats_all( slab_level_s * L, uint64_t sweeps ) {
@@ -148,6 +161,11 @@ namespace slabgpu {
 		const bool already_converged = !fixed && r_norm / denom < cfg->rtol; // cg.hpp:103
 		const uint64_t limit = already_converged ? 0 : planned;
 
+		// on a communicator, fixed-iteration solves combine r'r with the next r'z (iteration_enqueue)
+		const bool deferred = fixed && halo_has_comm( ctx );
+		if( deferred && limit > 0 ) {
+			SLAB_CUDA( cudaMemsetAsync( ctx->d_scalars + S_RR, 0, sizeof( double ), st ) ); // nothing to add in front of the first iteration
+		}
 		// iteration graph, cached per (x, config)
 		bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
@@ -160,7 +178,7 @@ namespace slabgpu {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
 				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
-				|| ws->key_scratch != ctx->scratch_gen;
+				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 );
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -175,7 +193,7 @@ namespace slabgpu {
 				try {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 					try {
-						iteration_enqueue( H, ws, x, cfg );
+						iteration_enqueue( H, ws, x, cfg, deferred );
 					} catch( ... ) {
 						cudaStreamEndCapture( st, &graph );
 						if( graph ) {
@@ -192,17 +210,36 @@ namespace slabgpu {
 					captured = true;
 				} catch( const Error & ) {
 					// With a communicator attached the iteration contains NCCL operations on two streams; if
-					// this driver/NCCL pair refuses to capture them, this rank enqueues the same operations
-					// launch by launch instead (the traffic on the wire is identical, so ranks may differ).
+					// this driver/NCCL pair refuses to capture them, the same operations are enqueued launch by
+					// launch instead — on EVERY rank: the ranks agree on that below.
 					if( !halo_has_comm( ctx ) ) {
 						throw;
 					}
 					cudaGetLastError();
+					if( ws->iter_exec ) {
+						cudaGraphExecDestroy( ws->iter_exec );
+					}
 					ws->iter_exec = nullptr;
-					ctx->use_graphs = 0;
-					graphs = false;
+					captured = false;
 				}
 				g_launch_count = before;
+				if( halo_has_comm( ctx ) ) {
+					// every rank must run the same mode (a graph replay and launch-by-launch enqueueing issue their
+					// collectives from different streams' points of view): the ranks agree on the number of failures
+					ensure_pinned( ctx, 1 );
+					ctx->h_pinned[ 0 ] = captured ? 0.0 : 1.0;
+					SLAB_CUDA( cudaMemcpyAsync( ctx->d_scalars + S_TMP, ctx->h_pinned, sizeof( double ), cudaMemcpyHostToDevice, st ) );
+					allreduce_slot( ctx, S_TMP );
+					if( read_scalar( ctx, S_TMP ) != 0.0 ) {
+						if( ws->iter_exec ) {
+							cudaGraphExecDestroy( ws->iter_exec );
+							ws->iter_exec = nullptr;
+						}
+						captured = false;
+						ctx->use_graphs = 0;
+						graphs = false;
+					}
+				}
 				if( captured ) {
 					ws->key_x = x->d;
 					ws->key_sweeps = cfg->sweeps;
@@ -211,6 +248,7 @@ namespace slabgpu {
 					ws->key_fused = ctx->fused_transfers;
 					ws->key_epoch = g_tuning_epoch;
 					ws->key_scratch = ctx->scratch_gen;
+					ws->key_deferred = deferred ? 1 : 0;
 				}
 			}
 		}
@@ -220,7 +258,7 @@ namespace slabgpu {
 				SLAB_CUDA( cudaGraphLaunch( ws->iter_exec, st ) );
 				count_launch( ws->iter_launches );
 			} else {
-				iteration_enqueue( H, ws, x, cfg );
+				iteration_enqueue( H, ws, x, cfg, deferred );
 			}
 			if( cfg->use_preconditioner ) {
 				vcycle_stats_all( H, cfg->sweeps );
@@ -231,6 +269,10 @@ namespace slabgpu {
 		if( fixed ) {
 			for( uint64_t iter = 1; iter <= limit; ++iter ) {
 				run_iteration();
+			}
+			if( deferred && limit > 0 ) { // the last iteration's r'r is still this rank's part
+				allreduce_slot( ctx, S_RR );
+				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, true );
 			}
 			if( limit > 0 ) {
 				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ws->d_hist_rr, limit * sizeof( double ), cudaMemcpyDeviceToHost,

@@ -89,7 +89,9 @@ namespace slabgpu {
 	constexpr uint64_t kDotChunk = 4096;  // parallel.hpp:70
 
 	// device scalar slots used by the CG driver (doubles in ctx->d_scalars)
-	enum Scalar { S_RHO = 0, S_RHO_PREV, S_PQ, S_RR, S_TMP, S_BB, S_COUNT = 16 };
+	// S_RHO and S_RR are neighbours: on a communicator r'z of an iteration and r'r of the one before travel in ONE
+	// allreduce of two doubles (cg.cu)
+	enum Scalar { S_RHO = 0, S_RR, S_RHO_PREV, S_PQ, S_TMP, S_BB, S_COUNT = 16 };
 
 	// Dictionary-coded companion of a SELL matrix (packed.cu). Every stored entry is replaced by one
 	// byte: the index of its (column - row, value) pair in a dictionary of at most 254 pairs found in
@@ -290,6 +292,7 @@ namespace slabgpu {
 		int key_precond = -1, key_dot = -1, key_fused = -1;
 		uint64_t key_epoch = ~uint64_t( 0 );
 		uint64_t key_scratch = ~uint64_t( 0 );
+		int key_deferred = -1;
 		uint64_t iter_launches = 0;
 		~CgWorkspace();
 	};
@@ -348,6 +351,7 @@ namespace slabgpu {
 	const uint8_t * halo_boundary_flags( const HaloPlan * plan );
 	extern int g_halo_overlap;
 	void allreduce_slot( slab_ctx_s * ctx, int slot ); // sum d_scalars[slot] over ranks, in place
+	void allreduce_slots( slab_ctx_s * ctx, int slot, int count ); // ... d_scalars[slot .. slot + count)
 	void dist_destroy( slab_ctx_s * ctx );
 
 	// ---- level.cu
@@ -372,7 +376,8 @@ namespace slabgpu {
 	// ---- ops (kernels.cu)
 	void op_set_all( slab_vec_s * v, double value );
 	void op_waxpby( slab_vec_s * w, double alpha, slab_vec_s * x, double beta, slab_vec_s * y );
-	void op_dot_to_slot( slab_vec_s * x, slab_vec_s * y, int slot ); // result -> ctx->d_scalars[slot]
+	// result -> ctx->d_scalars[slot]; reduce = false leaves this rank's part there (the caller combines allreduces)
+	void op_dot_to_slot( slab_vec_s * x, slab_vec_s * y, int slot, bool reduce = true );
 	double op_dot( slab_vec_s * x, slab_vec_s * y );
 	void op_mxv( slab_vec_s * y, slab_mask_s * mask, slab_mat_s * A, slab_vec_s * x, unsigned desc );
 

@@ -399,7 +399,7 @@ namespace slabgpu {
 		kern::waxpby( w->ctx->stream, w->d, alpha, x->d, beta, y->d, w->n );
 	}
 
-	void op_dot_to_slot( slab_vec_s * x, slab_vec_s * y, int slot ) {
+	void op_dot_to_slot( slab_vec_s * x, slab_vec_s * y, int slot, bool reduce ) {
 		if( x->n != y->n ) { // operations.hpp:63-65
 			fail( SLAB_ERR_DIMENSION_MISMATCH, "dot: vector lengths differ" );
 		}
@@ -412,7 +412,9 @@ namespace slabgpu {
 			kern::dot_tree( ctx->stream, x->d, y->d, x->n, ctx->sm_count, ctx->d_partials, ctx->d_counter,
 				ctx->d_scalars + slot );
 		}
-		allreduce_slot( ctx, slot ); // sum of the ranks' owned parts; no-op on one process
+		if( reduce ) {
+			allreduce_slot( ctx, slot ); // sum of the ranks' owned parts; no-op on one process
+		}
 	}
 
 	double op_dot( slab_vec_s * x, slab_vec_s * y ) {

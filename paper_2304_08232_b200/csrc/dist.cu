@@ -338,12 +338,16 @@ namespace slabgpu {
 		halo_exchange_plan( L->ctx, L->plan, v, color );
 	}
 
-	void allreduce_slot( slab_ctx_s * ctx, int slot ) {
+	void allreduce_slots( slab_ctx_s * ctx, int slot, int count ) {
 		if( ctx->dist == nullptr || ctx->dist->comm == nullptr ) {
 			return;
 		}
-		nccl_check( nccl().AllReduce( ctx->d_scalars + slot, ctx->d_scalars + slot, 1, kNcclFloat64, kNcclSum,
+		nccl_check( nccl().AllReduce( ctx->d_scalars + slot, ctx->d_scalars + slot, static_cast< size_t >( count ), kNcclFloat64, kNcclSum,
 			ctx->dist->comm, ctx->stream ), "ncclAllReduce" );
+	}
+
+	void allreduce_slot( slab_ctx_s * ctx, int slot ) {
+		allreduce_slots( ctx, slot, 1 );
 	}
 
 } // namespace slabgpu

@@ -881,6 +881,21 @@ namespace slabgpu {
 				*iter_counter = it + 1;
 			}
 
+			// the same bookkeeping one step late (cg.cu, solves on a communicator): the r'r an iteration leaves behind is
+			// only global after the NEXT iteration's combined allreduce, so iteration k records iteration k-1
+			__global__ void k_cg_record_deferred( const double * scalars, double * hist_rr, double * hist_pq, unsigned int * iter_counter, int last ) {
+				dep_trigger();
+				dep_wait();
+				const unsigned int it = *iter_counter;
+				if( it > 0u ) {
+					hist_rr[ it - 1u ] = scalars[ S_RR ];
+					hist_pq[ it - 1u ] = scalars[ S_PQ ];
+				}
+				if( !last ) {
+					*iter_counter = it + 1u;
+				}
+			}
+
 		} // namespace
 
 		// ================================================================ wrappers
@@ -1173,6 +1188,10 @@ namespace slabgpu {
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,
 			unsigned int * iter_counter ) {
 			launch( k_cg_record, 1, 1, st, scalars, hist_rr, hist_pq, iter_counter );
+		}
+
+		void cg_record_deferred( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq, unsigned int * iter_counter, bool last ) {
+			launch( k_cg_record_deferred, 1, 1, st, scalars, hist_rr, hist_pq, iter_counter, last ? 1 : 0 );
 		}
 
 	} // namespace kern

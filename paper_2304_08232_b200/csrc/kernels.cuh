@@ -114,6 +114,8 @@ namespace slabgpu {
 		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n, int sm_count, double * partials, unsigned int * counter );
 		// hist_rr[it] = rr, hist_pq[it] = pq, ++it
+		// iteration k-1's bookkeeping inside iteration k (it > 0 only; last: after the final iteration, no increment)
+		void cg_record_deferred( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq, unsigned int * iter_counter, bool last );
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,
 			unsigned int * iter_counter );
 

@@ -279,6 +279,33 @@ def test_single_rank_nccl_communicator_is_transparent(slab, ctx):
     assert got.residual_history == want.residual_history
     assert np.array_equal(got.solution.values(), want.solution.values())
     assert slab.dot(db, db) == slab.dot(b, b)
+    # On a communicator a fixed-iteration solve sends r'r together with the next iteration's r'z (one allreduce of two
+    # doubles) and writes an iteration's history entry one iteration late: same numbers, in both dot modes, with and
+    # without the iteration graph; a tolerance-driven solve keeps the immediate reductions.
+    for mode in (slab.DOT_TREE, slab.DOT_EXACT):
+        ctx.dot_mode = dctx.dot_mode = mode
+        try:
+            want_m = slab.cg_solve(plain, b, ctx.DenseVector(plain.n(), 0.0), cfg)
+            got_m = slab.cg_solve(h, db, dctx.DenseVector(h.n(), 0.0), cfg)
+            dctx.set_graphs(False)
+            eager = slab.cg_solve(h, db, dctx.DenseVector(h.n(), 0.0), cfg)
+            dctx.set_graphs(True)
+            tol = slab.CGConfig(max_iters=40, rtol=1e-9)
+            want_t = slab.cg_solve(plain, b, ctx.DenseVector(plain.n(), 0.0), tol)
+            got_t = slab.cg_solve(h, db, dctx.DenseVector(h.n(), 0.0), tol)
+        finally:
+            ctx.dot_mode = dctx.dot_mode = slab.DOT_EXACT
+        assert len(got_m.residual_history) == 13 and eager.residual_history == got_m.residual_history
+        assert got_t.converged and got_t.iterations == want_t.iterations
+        if mode == slab.DOT_EXACT:
+            assert got_m.residual_history == want_m.residual_history
+            assert np.array_equal(got_m.solution.values(), want_m.solution.values())
+            assert got_t.residual_history == want_t.residual_history
+        else:  # tree dots: the product's fused dot has another tree shape without the slab-staged kernel
+            w = np.array(want_m.residual_history)
+            assert np.max(np.abs(np.array(got_m.residual_history) - w) / w) <= 1e-10
+            w = np.array(want_t.residual_history)
+            assert np.max(np.abs(np.array(got_t.residual_history) - w) / w) <= 1e-10
 
 
 def test_full_size_two_rank_vcycle_equals_global_bitwise(slab, ctx):
