@@ -20,7 +20,11 @@
  *    in the reference's natural (x-fastest) ordering;
  *  - one context = one device + one stream; calls are asynchronous on that stream except
  *    those that return data to the host. A context is driven by one host thread at a time
- *    (operations.hpp:27-31: parallelism lives inside the primitives);
+ *    (operations.hpp:27-31: parallelism lives inside the primitives). Several contexts may be
+ *    driven by several threads concurrently; what they share process-wide is the launch counter
+ *    (atomic) and the tuning knobs of slab_set_tuning / slab_set_programmatic_launch, which are a
+ *    benchmarking interface: set them while no other thread is inside the library (they are read
+ *    without locks, and changing one invalidates every context's cached graphs at its next use);
  *  - there is NO CPU fallback: creating a context without a usable sm_100 GPU fails with
  *    SLAB_ERR_CUDA.
  */

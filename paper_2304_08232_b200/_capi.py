@@ -812,11 +812,19 @@ def cg_solve_host(hierarchy: ProblemLevel, b: np.ndarray, x0: np.ndarray, cfg: C
     """cg_solve with HOST buffers: upload b/x0, solve, download x — the end-to-end plugin call."""
     cc = _c_config(cfg, smoother_cfg)
     b, x0 = _f64(b), _f64(x0)
-    if b.size != x0.size:
+    n = hierarchy.n()
+    if b.size != n or x0.size != n:
         raise DimensionMismatch("cg_solve: vector lengths differ from the system size")
     hist = np.zeros(_history_len(cfg), dtype=np.float64)
     res = _CgResult()
-    x = out if out is not None else np.empty_like(b)
+    if out is not None:
+        # the library writes n doubles through this pointer: anything but a writable, contiguous float64 array of
+        # exactly n elements would be written past its end or into a temporary copy
+        if not isinstance(out, np.ndarray) or out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"] or not out.flags["WRITEABLE"]:
+            raise InvalidArgument("cg_solve_host: out must be a writable C-contiguous float64 numpy array")
+        if out.size != n:
+            raise DimensionMismatch("cg_solve_host: out must have as many elements as the system has rows")
+    x = out if out is not None else np.empty(n, dtype=np.float64)
     _check(_lib.slab_cg_solve_host(hierarchy._h, _ptr(b), _ptr(x0), b.size, C.byref(cc), _ptr(x), _ptr(hist),
                                    C.byref(res)))
     k = int(res.iterations)

@@ -188,7 +188,7 @@ namespace slabgpu {
 				ensure_partials( ctx, std::max< uint64_t >( std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
 					kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
 				cudaGraph_t graph = nullptr;
-				const uint64_t before = g_launch_count;
+				const uint64_t before = thread_launches();
 				bool captured = false;
 				try {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
@@ -203,7 +203,7 @@ namespace slabgpu {
 						throw;
 					}
 					SLAB_CUDA( cudaStreamEndCapture( st, &graph ) );
-					ws->iter_launches = g_launch_count - before;
+					ws->iter_launches = thread_launches() - before;
 					const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph, 0 );
 					cudaGraphDestroy( graph );
 					SLAB_CUDA( err );
@@ -222,7 +222,8 @@ namespace slabgpu {
 					ws->iter_exec = nullptr;
 					captured = false;
 				}
-				g_launch_count = before;
+				g_launch_count -= thread_launches() - before; // enqueued into the graph, not launched
+				thread_launches() = before;
 				if( halo_has_comm( ctx ) ) {
 					// every rank must run the same mode (a graph replay and launch-by-launch enqueueing issue their
 					// collectives from different streams' points of view): the ranks agree on the number of failures

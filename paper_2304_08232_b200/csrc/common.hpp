@@ -10,6 +10,7 @@
 //    colour (the Gauss-Seidel steps), each colour block padded to whole slices.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <memory>
@@ -59,7 +60,7 @@ namespace slabgpu {
 	extern int g_l2_window;
 	extern int64_t g_stream_rows;
 	extern int g_stream_variant;
-	extern uint64_t g_launch_count;
+	extern std::atomic< uint64_t > g_launch_count; // kernels launched by this process (all contexts)
 	extern int g_use_pdl; // chain kernels with programmatic dependent launch (default on)
 	extern int g_use_packed;   // run products and colour steps from the dictionary-coded matrix copy when one exists
 	extern int g_pack_build;   // build the dictionary-coded copy when a matrix is created
@@ -81,8 +82,15 @@ namespace slabgpu {
 	extern int64_t g_spmv_plane_min_rows; // ... for matrices of at least this many rows
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
+	// launches a thread has counted so far: a stream capture counts its enqueues here and takes them back from
+	// the process-wide counter afterwards (they run when the graph is replayed, and are counted then)
+	inline uint64_t & thread_launches() {
+		thread_local uint64_t count = 0;
+		return count;
+	}
 	inline void count_launch( uint64_t k = 1 ) {
 		g_launch_count += k;
+		thread_launches() += k;
 	}
 
 	constexpr int kSlice = 32;            // rows per SELL slice = one warp

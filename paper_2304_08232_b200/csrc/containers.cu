@@ -175,7 +175,9 @@ namespace slabgpu {
 				fail( SLAB_ERR_INVALID_ARGUMENT, "grid dimensions must all be at least 2, got " + std::to_string( nx ) + "x"
 					+ std::to_string( ny ) + "x" + std::to_string( nz ) );
 			}
-			if( nx * ny * nz >= ( uint64_t( 1 ) << 31 ) ) {
+			// (overflow-safe: a product that wraps around 2^64 must not slip under the limit)
+			const uint64_t limit = uint64_t( 1 ) << 31;
+			if( nx >= limit || ny >= limit || nz >= limit || nx > ( limit - 1 ) / ny || nx * ny > ( limit - 1 ) / nz ) {
 				fail( SLAB_ERR_INVALID_ARGUMENT, "grid too large for 32-bit column indices on one device" );
 			}
 		}

@@ -21,6 +21,8 @@
 //  * Vector gathers (x / z) are served by L1/L2.
 #include "kernels.cuh"
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include "common.hpp"
@@ -29,7 +31,7 @@
 
 namespace slabgpu {
 
-	uint64_t g_launch_count = 0;
+	std::atomic< uint64_t > g_launch_count{ 0 };
 	int g_use_pdl = 1;
 	// L2 persisting carve-out (set by slab_ctx_create from the device limits; 0 = unused)
 	size_t g_l2_persist_bytes = 0;
@@ -57,7 +59,7 @@ namespace slabgpu {
 			// Vector that the next launch should keep in the L2 persisting carve-out (the z of a fine-level
 			// colour step: every step gathers all of it while the matrix streams through). Consumed by the
 			// next launch() only.
-			const void * t_window_base = nullptr;
+			thread_local const void * t_window_base = nullptr;
 			size_t t_window_bytes = 0;
 
 			// launch with the programmatic-stream-serialization attribute (PDL)
@@ -324,7 +326,9 @@ namespace slabgpu {
 				const uint64_t nchunks = ( n + kDotChunk - 1 ) / kDotChunk;
 				const uint64_t chunk0 = static_cast< uint64_t >( blockIdx.x ) * cpb;
 				const int nmine = static_cast< int >( nchunks - chunk0 < static_cast< uint64_t >( cpb ) ? nchunks - chunk0 : cpb );
-				const int ntiles = static_cast< int >( kDotChunk ) / tile;
+				// tiles of the block's longest chunk (its first: only the last chunk of the vector is short)
+				const uint64_t longest = n - chunk0 * kDotChunk < kDotChunk ? n - chunk0 * kDotChunk : kDotChunk;
+				const int ntiles = static_cast< int >( ( longest + tile - 1 ) / tile );
 				const uint64_t begin = ( chunk0 + lane ) * kDotChunk; // this lane's chunk
 				const int len = lane < nmine ? static_cast< int >( n - begin < kDotChunk ? n - begin : kDotChunk ) : 0;
 				const bool aligned = ( ( reinterpret_cast< uintptr_t >( x ) | reinterpret_cast< uintptr_t >( y ) ) & 15 ) == 0;

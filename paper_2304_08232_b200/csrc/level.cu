@@ -208,6 +208,12 @@ namespace slabgpu {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "grid dimensions must all be at least 2, got " + std::to_string( nx ) + "x"
 				+ std::to_string( ny ) + "x" + std::to_string( nz ) );
 		}
+		{ // the row count must fit 32-bit column indices; checked without letting the product wrap
+			const uint64_t limit = uint64_t( 1 ) << 31;
+			if( nx >= limit || ny >= limit || nz >= limit || nx > ( limit - 1 ) / ny || nx * ny > ( limit - 1 ) / nz ) {
+				fail( SLAB_ERR_INVALID_ARGUMENT, "grid too large for 32-bit column indices on one device" );
+			}
+		}
 		if( levels < 1 ) {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "build_hierarchy: need at least one level" );
 		}
@@ -703,7 +709,7 @@ namespace slabgpu {
 				L->vcycle_exec = nullptr;
 			}
 			cudaGraph_t graph = nullptr;
-			const uint64_t launches_before = g_launch_count;
+			const uint64_t launches_before = thread_launches();
 			SLAB_CUDA( cudaStreamBeginCapture( ctx->stream, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 			try {
 				halo_exchange( L, z, -1 );
@@ -716,8 +722,9 @@ namespace slabgpu {
 				throw;
 			}
 			SLAB_CUDA( cudaStreamEndCapture( ctx->stream, &graph ) );
-			L->vcycle_launches = g_launch_count - launches_before;
-			g_launch_count = launches_before;
+			L->vcycle_launches = thread_launches() - launches_before;
+			g_launch_count -= L->vcycle_launches; // enqueued into the graph, not launched
+			thread_launches() = launches_before;
 			const cudaError_t err = cudaGraphInstantiate( &L->vcycle_exec, graph, 0 );
 			cudaGraphDestroy( graph );
 			SLAB_CUDA( err );

@@ -252,10 +252,14 @@ def test_hierarchy_shape_and_colors(slab, ctx, small):
 
 
 def test_hierarchy_rejection_rules(slab, ctx):
-    """test_problem.cpp:223-236"""
-    for dims, levels in [((1, 4, 4), 1), ((4, 4, 4), 0), ((6, 4, 4), 3), ((4, 4, 4), 3), ((12, 12, 10), 3)]:
+    """test_problem.cpp:223-236; and dimensions whose product wraps around 2^64 must not slip under the size limit"""
+    for dims, levels in [((1, 4, 4), 1), ((4, 4, 4), 0), ((6, 4, 4), 3), ((4, 4, 4), 3), ((12, 12, 10), 3),
+                         ((1 << 22, 1 << 22, 1 << 22), 1), ((1 << 32, 1 << 32, 2), 1), ((1 << 31, 2, 2), 1)]:
         with pytest.raises(slab.InvalidArgument):
             ctx.build_hierarchy(dims, levels)
+    for dims in [(1 << 22, 1 << 22, 1 << 22), (1 << 40, 1 << 24, 4)]:
+        with pytest.raises(slab.InvalidArgument):
+            ctx.build_matrix(dims)
 
 
 def test_general_level_coloring_matches_oracle_greedy(slab, ctx, oracle):

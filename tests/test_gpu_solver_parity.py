@@ -214,3 +214,50 @@ def test_odd_coarse_grid_hierarchy_matches_oracle(slab, ctx, oracle):
     ores = oracle.cg_solve(oh, ob, np.zeros(oh.n), max_iters=15, fixed_iterations=15)
     assert res.residual_history == ores.residual_history
     assert np.array_equal(res.solution.values(), ores.solution)
+
+
+def test_alternating_hierarchies_on_one_context(slab, ctx):
+    """A cached iteration graph must never be replayed with a stale pointer to the context's reduction scratch
+    (ADVICE r01): a small hierarchy is solved, then a larger one whose fused product dot needs more partials (the scratch
+    is reallocated), then the small one again — with a vector allocated in between that could take the freed block.
+    Every solve must reproduce its first history bit for bit."""
+    fresh = slab.Context(0)
+    cfg = slab.CGConfig(max_iters=8, fixed_iterations=8)
+
+    def problem(dims):
+        h = fresh.build_hierarchy(dims, 3)
+        b = fresh.DenseVector(h.n())
+        slab.mxv(b, h.A, fresh.DenseVector(h.n(), 1.0))
+        return h, b, fresh.DenseVector(h.n(), 0.0), fresh.DenseVector(h.n())
+
+    for mode in (slab.DOT_TREE, slab.DOT_EXACT):
+        fresh.dot_mode = mode
+        small, large = problem((32, 32, 32)), problem((112, 104, 96))
+        first_small = slab.cg_solve(small[0], small[1], small[2], cfg, out=small[3]).residual_history
+        first_large = slab.cg_solve(large[0], large[1], large[2], cfg, out=large[3]).residual_history
+        filler = [fresh.DenseVector(40000, 1.0) for _ in range(4)]  # may land in the block the old scratch left
+        again_small = slab.cg_solve(small[0], small[1], small[2], cfg, out=small[3]).residual_history
+        again_large = slab.cg_solve(large[0], large[1], large[2], cfg, out=large[3]).residual_history
+        assert again_small == first_small and again_large == first_large
+        assert all(np.all(v.values() == 1.0) for v in filler)
+
+
+def test_host_entry_point_rejects_unusable_output_buffers(slab, ctx):
+    """cg_solve_host hands `out` to the library as a raw pointer: wrong dtype, strides, size or a read-only
+    array must be refused before anything is written."""
+    h = ctx.build_hierarchy((8, 8, 8), 2)
+    n = h.n()
+    b = np.ones(n)
+    cfg = slab.CGConfig(max_iters=2, fixed_iterations=2)
+    good = np.empty(n)
+    slab.cg_solve_host(h, b, np.zeros(n), cfg, out=good)
+    assert np.all(np.isfinite(good))
+    for bad in (np.empty(n, dtype=np.float32), np.empty(2 * n)[::2], np.empty(n - 1), np.empty(n + 5)):
+        with pytest.raises((slab.InvalidArgument, slab.DimensionMismatch)):
+            slab.cg_solve_host(h, b, np.zeros(n), cfg, out=bad)
+    frozen = np.empty(n)
+    frozen.flags.writeable = False
+    with pytest.raises(slab.InvalidArgument):
+        slab.cg_solve_host(h, b, np.zeros(n), cfg, out=frozen)
+    with pytest.raises(slab.DimensionMismatch):
+        slab.cg_solve_host(h, np.ones(n + 1), np.zeros(n + 1), cfg)
