@@ -121,6 +121,10 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_use_planes = value ? 1 : 0;
 		} else if( k == "dot_cpb" ) {
 			g_dot_cpb = static_cast< int >( value );
+		} else if( k == "plane_pad_lines" ) {
+			g_plane_pad_lines = static_cast< int >( value );
+		} else if( k == "plane_warp_sync" ) {
+			g_plane_warp_sync = value ? 1 : 0;
 		} else if( k == "spmv_planes" ) {
 			g_use_spmv_planes = value ? 1 : 0;
 		} else if( k == "spmv_plane_min_rows" ) {

@@ -82,6 +82,8 @@ namespace slabgpu {
 	extern int64_t g_spmv_plane_min_rows; // ... for matrices of at least this many rows
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
+	extern int g_plane_pad_lines;     // plane.cu: pad lines to a divisor of 32 threads (0 never, 1 up to 35 % idle, 2 always)
+	extern int g_plane_warp_sync;     // plane.cu: warp instead of block barriers between the x-parity colours of a line (default 1)
 	// launches a thread has counted so far: a stream capture counts its enqueues here and takes them back from
 	// the process-wide counter afterwards (they run when the graph is replayed, and are counted then)
 	inline uint64_t & thread_launches() {
