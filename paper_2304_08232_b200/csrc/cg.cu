@@ -61,8 +61,13 @@ namespace slabgpu {
 			slab_vec_s * p = ws->p.get();
 			slab_vec_s * q = ws->q.get();
 			if( cfg->use_preconditioner ) {
-				op_set_all( z, 0.0 ); // cg.hpp:111
-				mg_vcycle_enqueue( H, z, r, cfg->sweeps, false );
+				// cg.hpp:111: the V-cycle starts from z = 0. Levels that run the plane phases take that as a flag of their
+				// first phase (nothing is read, every slab is zeros) instead of a pass that writes the zeros
+				const bool hint = mg_vcycle_accepts_zero_guess( H );
+				if( !hint ) {
+					op_set_all( z, 0.0 );
+				}
+				mg_vcycle_enqueue( H, z, r, cfg->sweeps, false, hint );
 			} else {
 				op_waxpby( z, 1.0, r, 0.0, r ); // cg.hpp:114
 			}

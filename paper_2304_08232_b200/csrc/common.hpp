@@ -376,7 +376,9 @@ namespace slabgpu {
 	void restrict_vector( slab_level_s * L, slab_vec_s * v_fine, slab_vec_s * out );
 	void refine_and_add( slab_level_s * L, slab_vec_s * z, slab_vec_s * z_c );
 	void mg_vcycle( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
-	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats );
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess = false );
+	// does the V-cycle rooted at L take the "z is zero" hint on its first phase (so that the caller need not zero z)?
+	bool mg_vcycle_accepts_zero_guess( const slab_level_s * L );
 	// everything mg_vcycle_enqueue needs that may allocate or copy (phase lists of the persistent kernel,
 	// lazily built transposes): must run before stream capture begins
 	void mg_vcycle_prepare( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );

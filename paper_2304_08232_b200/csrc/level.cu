@@ -427,7 +427,7 @@ namespace slabgpu {
 			if( planes_usable( L ) ) {
 				// plane.cu: even planes (colours 0-3), odd planes (4-7, 7-4), even planes (3-0); every phase out of place
 				double * const zs = L->zs->d;
-				plane_phase_enqueue( L, 0, 1, z->d, z->d, zs, zs, r, first_flags & 1 );       // z -> zs, odd planes copied along
+				plane_phase_enqueue( L, 0, 1, z->d, z->d, zs, zs, r, first_flags & ( 1 | 8 ) ); // z -> zs, odd planes copied along
 				plane_phase_enqueue( L, 1, 0, zs, zs, z->d, nullptr, r, 0 );                  // odd planes: zs -> z
 				plane_phase_enqueue( L, 2, 0, zs, z->d, z->d, nullptr, r, last_flags & 2 );   // even planes: zs (+ odd planes of z) -> z
 				return;
@@ -469,9 +469,11 @@ namespace slabgpu {
 			}
 		}
 
-		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps ) { // smoother.hpp:108-111
+		// zero_guess: z is known to be zero on entry; levels that run the plane phases then do not read it in the first
+		// phase of the first sweep (first_flags bit 3), every other path ignores the hint
+		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool zero_guess = false ) { // smoother.hpp:108-111
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				sweep_pair_enqueue( L, z, r );
+				sweep_pair_enqueue( L, z, r, sweep == 0 && zero_guess && planes_usable( L ) ? 8 : 0, 0 );
 			}
 		}
 	} // namespace
@@ -594,7 +596,13 @@ namespace slabgpu {
 	}
 
 	// multigrid.hpp:87-116, enqueue only (no checks, no host synchronisation): safe under stream capture
-	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats ) {
+	bool mg_vcycle_accepts_zero_guess( const slab_level_s * L ) {
+		const slab_ctx_s * ctx = L->ctx;
+		return !ctx->profiling && planes_usable( L ) && ( !L->coarser || ( ctx->fused_transfers && L->is_stencil ) );
+	}
+
+	// zero_guess: the caller knows z to be zero (cg.hpp:111; the coarse guesses of multigrid.hpp:104)
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess ) {
 		slab_ctx_s * ctx = L->ctx;
 		if( ctx->profiling ) {
 			// the reference's instrumentation (multigrid.hpp:92-114, smoother.hpp:79-98): per-level V-cycle
@@ -642,7 +650,7 @@ namespace slabgpu {
 			return;
 		}
 		if( !L->coarser ) {
-			symmetric_enqueue( L, z, r, sweeps );
+			symmetric_enqueue( L, z, r, sweeps, zero_guess );
 			if( count_stats ) {
 				L->stats.nnz_visited += 2 * sweeps * L->nnz;
 			}
@@ -669,7 +677,7 @@ namespace slabgpu {
 			const bool fuse_residual = planes_usable( L ) || kern::gs_color_step_can_fuse_residual( L->colorA, static_cast< int64_t >( L->color_size[ 0 ] ) );
 			const bool ghosts = L->z_c->n_alloc > L->z_c->n; // distributed: the ghost tail must be zeroed too
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				sweep_pair_enqueue( L, z, r, 0, sweep + 1 == sweeps && fuse_residual ? 2 : 0 );
+				sweep_pair_enqueue( L, z, r, sweep == 0 && zero_guess && planes_usable( L ) ? 8 : 0, sweep + 1 == sweeps && fuse_residual ? 2 : 0 );
 			}
 			if( !fuse_residual ) {
 				kern::residual_restrict( ctx->stream, L->colorA, L->d_rows,
@@ -678,7 +686,7 @@ namespace slabgpu {
 			if( ghosts ) {
 				op_set_all( L->z_c.get(), 0.0 );
 			}
-			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats );
+			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats, true ); // z_c was zeroed above
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
 				sweep_pair_enqueue( L, z, r, sweep == 0 ? 1 : 0, 0 );
 			}
