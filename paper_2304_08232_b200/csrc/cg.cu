@@ -60,6 +60,7 @@ namespace slabgpu {
 			slab_vec_s * z = ws->z.get();
 			slab_vec_s * p = ws->p.get();
 			slab_vec_s * q = ws->q.get();
+			bool fused_rz = false;
 			if( cfg->use_preconditioner ) {
 				// cg.hpp:111: the V-cycle starts from z = 0. Levels that run the plane phases take that as a flag of their
 				// first phase (nothing is read, every slab is zeros) instead of a pass that writes the zeros
@@ -67,11 +68,19 @@ namespace slabgpu {
 				if( !hint ) {
 					op_set_all( z, 0.0 );
 				}
-				mg_vcycle_enqueue( H, z, r, cfg->sweeps, false, hint );
+				// tree-dot mode: r'z (cg.hpp:116) rides on the last two plane phases of the V-cycle, which hold r_i and the
+				// final z_i of every row in registers: one pass over r and z less
+				fused_rz = hint && ctx->dot_mode == SLAB_DOT_TREE && g_fuse_rz != 0 && g_plane_rows != 2
+					&& ( g_fuse_rz >= 2 || H->n >= ( uint64_t( 1 ) << 19 ) ); // below that the fold's own launch costs more than the dot
+				mg_vcycle_enqueue( H, z, r, cfg->sweeps, false, hint, fused_rz );
 			} else {
 				op_waxpby( z, 1.0, r, 0.0, r ); // cg.hpp:114
 			}
-			op_dot_to_slot( r, z, S_RHO, !deferred );                             // cg.hpp:116
+			if( fused_rz ) {
+				kern::sum_partials( st, ctx->d_partials, mg_vcycle_rz_partials( H ), ctx->d_scalars + S_RHO );
+			} else {
+				op_dot_to_slot( r, z, S_RHO, !deferred );                             // cg.hpp:116
+			}
 			if( deferred ) {
 				allreduce_slots( ctx, S_RHO, 2 ); // r'z of this iteration, r'r of the one before (0 in front of the first)
 			}
@@ -178,7 +187,7 @@ namespace slabgpu {
 		}
 		// reduction scratch for every dot shape used below (allocation is illegal while capturing)
 		ensure_partials( ctx, std::max< uint64_t >( std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
-			kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
+			kern::dot_tree_blocks( n, ctx->sm_count ) ), std::max< uint64_t >( kern::spmv_dot_blocks( static_cast< int64_t >( n ) ), 4096 ) ) );
 		if( graphs && limit > 0 ) {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
@@ -191,7 +200,7 @@ namespace slabgpu {
 				}
 				// reduction scratch must exist before capture (allocation is illegal while capturing)
 				ensure_partials( ctx, std::max< uint64_t >( std::max< uint64_t >( ( n + kDotChunk - 1 ) / kDotChunk,
-					kern::dot_tree_blocks( n, ctx->sm_count ) ), kern::spmv_dot_blocks( static_cast< int64_t >( n ) ) ) );
+					kern::dot_tree_blocks( n, ctx->sm_count ) ), std::max< uint64_t >( kern::spmv_dot_blocks( static_cast< int64_t >( n ) ), 4096 ) ) );
 				cudaGraph_t graph = nullptr;
 				const uint64_t before = thread_launches();
 				bool captured = false;

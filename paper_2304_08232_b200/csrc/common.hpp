@@ -82,6 +82,7 @@ namespace slabgpu {
 	extern int64_t g_spmv_plane_min_rows; // ... for matrices of at least this many rows
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
+	extern int g_fuse_rz;             // cg.cu: r'z on the last plane phases of the V-cycle in tree-dot mode (default 1)
 	extern int g_plane_pad_lines;     // plane.cu: pad lines to a divisor of 32 threads (0 never, 1 up to 35 % idle, 2 always)
 	extern int g_plane_warp_sync;     // plane.cu: warp instead of block barriers between the x-parity colours of a line (default 1)
 	// launches a thread has counted so far: a stream capture counts its enqueues here and takes them back from
@@ -376,7 +377,9 @@ namespace slabgpu {
 	void restrict_vector( slab_level_s * L, slab_vec_s * v_fine, slab_vec_s * out );
 	void refine_and_add( slab_level_s * L, slab_vec_s * z, slab_vec_s * z_c );
 	void mg_vcycle( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps );
-	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess = false );
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess = false,
+		bool fuse_rz = false );
+	uint64_t mg_vcycle_rz_partials( const slab_level_s * L ); // partials the fused r'z leaves in ctx->d_partials
 	// does the V-cycle rooted at L take the "z is zero" hint on its first phase (so that the caller need not zero z)?
 	bool mg_vcycle_accepts_zero_guess( const slab_level_s * L );
 	// everything mg_vcycle_enqueue needs that may allocate or copy (phase lists of the persistent kernel,

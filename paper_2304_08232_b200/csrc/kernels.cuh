@@ -94,7 +94,9 @@ namespace slabgpu {
 		bool gs_planes_usable( const BoxTile & T, int64_t rows, int sm_count );
 		void gs_planes_prepare(); // function attributes; call outside stream capture
 		void gs_planes( cudaStream_t st, int sm_count, const BoxTile & T, int kind, int pass, const double * own_in, const double * nb_in,
-			double * own_out, double * pass_out, const double * r, int flags, const double * src, double * out, double * zero );
+			double * own_out, double * pass_out, const double * r, int flags, const double * src, double * out, double * zero,
+			double * dot_partials = nullptr ); // flags bit 4: one partial of r'z per block (kinds 1 and 2)
+		uint64_t gs_planes_blocks( const BoxTile & T, int kind, int sm_count );
 
 		// ---- plane_spmv.cu: y = A x of a regular box matrix, x staged through shared memory (every staged value read once
 		// per thread); dot_out != nullptr: x'(A x) in a fixed tree (dot_partials: spmv_planes_blocks doubles)

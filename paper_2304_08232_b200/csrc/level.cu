@@ -375,8 +375,13 @@ namespace slabgpu {
 
 		void plane_phase_enqueue( slab_level_s * L, int kind, int pass, const double * own_in, const double * nb_in, double * own_out,
 			double * pass_out, slab_vec_s * r, int flags ) {
+			// flags bit 4: r'z partials, phase B's blocks first, phase C's behind them (cg.cu folds them in that order)
+			double * dot_partials = nullptr;
+			if( flags & 16 ) {
+				dot_partials = L->ctx->d_partials + ( kind == 2 ? kern::gs_planes_blocks( L->tile, 1, L->ctx->sm_count ) : 0 );
+			}
 			kern::gs_planes( L->ctx->stream, L->ctx->sm_count, L->tile, kind, pass, own_in, nb_in, own_out, pass_out, r->d, flags,
-				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr );
+				( flags & 1 ) ? L->z_c->d : nullptr, ( flags & 2 ) ? L->r_c->d : nullptr, ( flags & 2 ) ? L->z_c->d : nullptr, dot_partials );
 		}
 
 		void forward_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r ) { // smoother.hpp:80-82
@@ -428,8 +433,8 @@ namespace slabgpu {
 				// plane.cu: even planes (colours 0-3), odd planes (4-7, 7-4), even planes (3-0); every phase out of place
 				double * const zs = L->zs->d;
 				plane_phase_enqueue( L, 0, 1, z->d, z->d, zs, zs, r, first_flags & ( 1 | 8 ) ); // z -> zs, odd planes copied along
-				plane_phase_enqueue( L, 1, 0, zs, zs, z->d, nullptr, r, 0 );                  // odd planes: zs -> z
-				plane_phase_enqueue( L, 2, 0, zs, z->d, z->d, nullptr, r, last_flags & 2 );   // even planes: zs (+ odd planes of z) -> z
+				plane_phase_enqueue( L, 1, 0, zs, zs, z->d, nullptr, r, last_flags & 16 );    // odd planes: zs -> z
+				plane_phase_enqueue( L, 2, 0, zs, z->d, z->d, nullptr, r, last_flags & ( 2 | 16 ) ); // even planes: zs (+ odd planes of z) -> z
 				return;
 			}
 			// small level on one process: the whole pair of sweeps in one launch (sweep_cluster.cu), same steps
@@ -471,9 +476,11 @@ namespace slabgpu {
 
 		// zero_guess: z is known to be zero on entry; levels that run the plane phases then do not read it in the first
 		// phase of the first sweep (first_flags bit 3), every other path ignores the hint
-		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool zero_guess = false ) { // smoother.hpp:108-111
+		// fuse_rz: the last sweep also leaves the partials of r'z behind (last_flags bit 4; plane phases only)
+		void symmetric_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool zero_guess = false, bool fuse_rz = false ) { // smoother.hpp:108-111
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				sweep_pair_enqueue( L, z, r, sweep == 0 && zero_guess && planes_usable( L ) ? 8 : 0, 0 );
+				sweep_pair_enqueue( L, z, r, sweep == 0 && zero_guess && planes_usable( L ) ? 8 : 0,
+					sweep + 1 == sweeps && fuse_rz && planes_usable( L ) ? 16 : 0 );
 			}
 		}
 	} // namespace
@@ -602,7 +609,13 @@ namespace slabgpu {
 	}
 
 	// zero_guess: the caller knows z to be zero (cg.hpp:111; the coarse guesses of multigrid.hpp:104)
-	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess ) {
+	uint64_t mg_vcycle_rz_partials( const slab_level_s * L ) {
+		return kern::gs_planes_blocks( L->tile, 1, L->ctx->sm_count ) + kern::gs_planes_blocks( L->tile, 2, L->ctx->sm_count );
+	}
+
+	// fuse_rz: the last phases of the last sweep leave the partials of r'z in the context's reduction scratch
+	// (only where mg_vcycle_accepts_zero_guess holds; cg.cu folds them)
+	void mg_vcycle_enqueue( slab_level_s * L, slab_vec_s * z, slab_vec_s * r, uint64_t sweeps, bool count_stats, bool zero_guess, bool fuse_rz ) {
 		slab_ctx_s * ctx = L->ctx;
 		if( ctx->profiling ) {
 			// the reference's instrumentation (multigrid.hpp:92-114, smoother.hpp:79-98): per-level V-cycle
@@ -650,7 +663,7 @@ namespace slabgpu {
 			return;
 		}
 		if( !L->coarser ) {
-			symmetric_enqueue( L, z, r, sweeps, zero_guess );
+			symmetric_enqueue( L, z, r, sweeps, zero_guess, fuse_rz );
 			if( count_stats ) {
 				L->stats.nnz_visited += 2 * sweeps * L->nnz;
 			}
@@ -688,7 +701,7 @@ namespace slabgpu {
 			}
 			mg_vcycle_enqueue( L->coarser.get(), L->z_c.get(), L->r_c.get(), sweeps, count_stats, true ); // z_c was zeroed above
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
-				sweep_pair_enqueue( L, z, r, sweep == 0 ? 1 : 0, 0 );
+				sweep_pair_enqueue( L, z, r, sweep == 0 ? 1 : 0, sweep + 1 == sweeps && fuse_rz && planes_usable( L ) ? 16 : 0 );
 			}
 		}
 		if( count_stats ) {

@@ -139,3 +139,31 @@ def test_solve_history_bitwise_through_planes(slab, ctx, tuning):
     slab.mxv(b, h.A, ctx.DenseVector(h.n(), 1.0))
     res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), slab.CGConfig(max_iters=50, fixed_iterations=50))
     assert res.residual_history == gold["residual_history"]
+
+
+def test_fused_rz_dot_and_zero_guess_keep_the_history(slab, ctx, tuning):
+    """tree-dot mode: r'z on the last two plane phases of the V-cycle (cg.hpp:116 fused; another tree shape, so 1e-12
+    against the separate dot), and the V-cycle's zero initial guess taken as a flag of the first phase (bit-identical:
+    exact-dot mode reproduces the reference's golden history through it)"""
+    from paper_2304_08232_b200 import _capi
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "history_64.json")))
+    want = np.array(gold["residual_history"])
+    h = ctx.build_hierarchy((64, 64, 64), 4)
+    b = ctx.DenseVector(h.n())
+    slab.mxv(b, h.A, ctx.DenseVector(h.n(), 1.0))
+    cfg = slab.CGConfig(max_iters=50, fixed_iterations=50)
+    ctx.dot_mode = slab.DOT_EXACT
+    res = slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), cfg)
+    assert res.residual_history == gold["residual_history"]
+    got = {}
+    try:
+        ctx.dot_mode = slab.DOT_TREE
+        for mode in (2, 0):
+            _capi.set_tuning("fuse_rz", mode)
+            got[mode] = np.array(slab.cg_solve(h, b, ctx.DenseVector(h.n(), 0.0), cfg).residual_history)
+    finally:
+        _capi.set_tuning("fuse_rz", 1)
+        ctx.dot_mode = slab.DOT_EXACT
+    assert np.max(np.abs(got[2] - got[0]) / got[0]) <= 1e-12
+    assert np.max(np.abs(got[2] - want) / want) <= 1e-10
