@@ -121,6 +121,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_use_planes = value ? 1 : 0;
 		} else if( k == "dot_cpb" ) {
 			g_dot_cpb = static_cast< int >( value );
+		} else if( k == "plane_autotune" ) {
+			g_plane_autotune = value ? 1 : 0;
 		} else if( k == "fuse_rz" ) {
 			g_fuse_rz = static_cast< int >( value ); // 0 off, 1 for systems of at least 2^19 rows, 2 always
 		} else if( k == "plane_pad_lines" ) {

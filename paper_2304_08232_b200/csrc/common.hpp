@@ -82,6 +82,7 @@ namespace slabgpu {
 	extern int64_t g_spmv_plane_min_rows; // ... for matrices of at least this many rows
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
+	extern int g_plane_autotune;      // plane.cu: measure proposed tile shapes at level creation (default 1)
 	extern int g_fuse_rz;             // cg.cu: r'z on the last plane phases of the V-cycle in tree-dot mode (default 1)
 	extern int g_plane_pad_lines;     // plane.cu: pad lines to a divisor of 32 threads (0 never, 1 up to 35 % idle, 2 always)
 	extern int g_plane_warp_sync;     // plane.cu: warp instead of block barriers between the x-parity colours of a line (default 1)
@@ -165,6 +166,8 @@ namespace slabgpu {
 		// every row stores exactly the offsets that stay inside the box, all 27 values are finite: the kernels of
 		// plane.cu need no masks then (zero-padded slabs stand in for the absent neighbours)
 		bool regular = false;
+		// plane.cu: tile shape (ty, cz, ns) of phases A, B, C as measured when the level was built (0: not measured)
+		int tuned[ 5 ][ 3 ] = { { 0 } };
 		void release();
 		bool usable() const {
 			return masks != nullptr;

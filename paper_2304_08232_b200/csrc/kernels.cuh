@@ -97,6 +97,8 @@ namespace slabgpu {
 			double * own_out, double * pass_out, const double * r, int flags, const double * src, double * out, double * zero,
 			double * dot_partials = nullptr ); // flags bit 4: one partial of r'z per block (kinds 1 and 2)
 		uint64_t gs_planes_blocks( const BoxTile & T, int kind, int sm_count );
+		// times the tile shapes the cost models propose and keeps the fastest in T (z, zs, r: scratch vectors, overwritten)
+		void gs_planes_tune( cudaStream_t st, int sm_count, BoxTile & T, double * z, double * zs, double * r );
 
 		// ---- plane_spmv.cu: y = A x of a regular box matrix, x staged through shared memory (every staged value read once
 		// per thread); dot_out != nullptr: x'(A x) in a fixed tree (dot_partials: spmv_planes_blocks doubles)

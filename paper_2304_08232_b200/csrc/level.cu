@@ -197,6 +197,14 @@ namespace slabgpu {
 				n_coarse = L->R->nrows;
 			}
 			alloc_scratch( L.get(), n_coarse );
+			if( L->planes_ok ) {
+				// the level measures the tile shapes its cost models propose for the three phases of a sweep (plane.cu)
+				std::unique_ptr< slab_vec_s > tmp( vec_new( ctx, L->n, 0.0 ) );
+				kern::gs_planes_tune( ctx->stream, ctx->sm_count, L->tile, tmp->d, L->zs->d, L->f->d );
+				kern::fill( ctx->stream, L->zs->d, L->n, 0.0 );
+				kern::fill( ctx->stream, L->f->d, L->n, 0.0 );
+				SLAB_CUDA( cudaStreamSynchronize( ctx->stream ) ); // tmp goes away
+			}
 			return L.release();
 		}
 
