@@ -254,73 +254,44 @@ namespace slabgpu {
 				return acc;
 			}
 
-			// One LANE per chunk, one WARP per SM. A chain of 4096 dependent additions costs 4096 x 8.8 cycles whoever
-			// runs it, and a warp instruction with one active lane takes the FP64 pipe's issue slot like a full one — so
-			// the chunks an SM is responsible for ride in the lanes of ONE warp (lane c adds chunk c: up to 32 chains per
-			// instruction, every step at the bare latency of the addition). The operands come by the bulk-async copy
-			// engine: each lane issues the copies of its own chunk's next tiles of x and y (two contiguous pieces per
-			// tile) into a ring of stages, completion counted on the stage's mbarrier, two stages in flight while the
-			// third is consumed — bytes in flight without a register or a loader warp. Rows of a stage are `pitch`
-			// doubles apart (tile + 2: 16-byte aligned for the copies, and the lanes' reads spread over the banks). The
-			// products are rounded on their own (operations.hpp:74) sixteen ahead of the additions that consume them. The
-			// block that finishes last adds the per-chunk partials in chunk order (operations.hpp:84-90).
+			// One LANE per chunk. A chain of 4096 dependent additions costs 4096 x 8.8 cycles whoever runs it, and a warp
+			// instruction with one active lane takes the FP64 pipe's issue slot like a full one — so the chunks an SM is
+			// responsible for ride in the lanes of ONE warp (lane c adds chunk c: up to 32 chains per instruction), and
+			// that warp does nothing but read a product and add it: every other instruction in it costs chain time (the
+			// multiply next to the add nearly doubled it). The block's other three warps sit on the other three
+			// sub-partitions and feed it: the operands arrive by the bulk-async copy engine (each chunk's next tiles of x
+			// and y, two contiguous pieces per tile, into a three-stage ring, completion counted on the stage's
+			// mbarrier), the converter warps round the products on their own (operations.hpp:74) into a two-deep ring of
+			// product tiles, and full/empty mbarriers hand the tiles over. Rows of the rings are tile + 2 (raw: 16-byte
+			// aligned for the copies) and tile + 1 (products: the lanes' reads fall into different banks) doubles apart.
+			// The block that finishes last adds the per-chunk partials in chunk order (operations.hpp:84-90).
 			constexpr int kDotStages = 3;
+			constexpr int kDotThreads = 128; // warp 0 adds; warps 1..3 copy and multiply
 
-			// acc + x[0] y[0] + x[1] y[1] + ... left to right for ONE thread; the products of the next 16 elements are in
-			// registers before the current 16 are added (two register sets that swap roles statically)
-			__device__ __forceinline__ double chain_prod( const double * px, const double * py, int count, double acc ) {
-				constexpr int kStep = 16;
-				double ra[ kStep ], rb[ kStep ];
-				#pragma unroll
-				for( int k = 0; k < kStep; ++k ) {
-					ra[ k ] = k < count ? __dmul_rn( px[ k ], py[ k ] ) : 0.0;
-				}
-				int i = 0;
-				for( ; i + 2 * kStep <= count; i += 2 * kStep ) {
-					#pragma unroll
-					for( int k = 0; k < kStep; ++k ) {
-						rb[ k ] = __dmul_rn( px[ i + kStep + k ], py[ i + kStep + k ] );
-					}
-					#pragma unroll
-					for( int k = 0; k < kStep; ++k ) {
-						acc = __dadd_rn( acc, ra[ k ] );
-					}
-					#pragma unroll
-					for( int k = 0; k < kStep; ++k ) {
-						ra[ k ] = i + 2 * kStep + k < count ? __dmul_rn( px[ i + 2 * kStep + k ], py[ i + 2 * kStep + k ] ) : 0.0;
-					}
-					#pragma unroll
-					for( int k = 0; k < kStep; ++k ) {
-						acc = __dadd_rn( acc, rb[ k ] );
-					}
-				}
-				#pragma unroll
-				for( int k = 0; k < kStep; ++k ) {
-					if( i + k < count ) {
-						acc = __dadd_rn( acc, ra[ k ] );
-					}
-				}
-				for( int j = i + kStep; j < count; ++j ) {
-					acc = __dadd_rn( acc, __dmul_rn( px[ j ], py[ j ] ) );
-				}
-				return acc;
-			}
-
-			__global__ void __launch_bounds__( 32 ) k_dot_exact( const double * x, const double * y, uint64_t n, int cpb, int tile, double * partials,
+			__global__ void __launch_bounds__( kDotThreads ) k_dot_exact( const double * x, const double * y, uint64_t n, int cpb, int tile, double * partials,
 				unsigned int * counter, double * out ) {
 				extern __shared__ __align__( 128 ) unsigned char dot_smem[];
-				uint64_t * const full = reinterpret_cast< uint64_t * >( dot_smem );
-				double * const stage0 = reinterpret_cast< double * >( dot_smem + 128 ); // [kDotStages][2][cpb][pitch]
-				const int lane = threadIdx.x;
-				const int pitch = tile + 2;
+				uint64_t * const full_raw = reinterpret_cast< uint64_t * >( dot_smem );     // [kDotStages]
+				uint64_t * const full_prod = full_raw + kDotStages;                          // [2]
+				uint64_t * const empty_prod = full_prod + 2;                                 // [2]
+				__shared__ bool is_last;
+				const int t = threadIdx.x;
+				const int lane = t & 31;
+				const int pitch = tile + 2, ppitch = tile + 1;
 				const size_t stage_elems = static_cast< size_t >( 2 ) * cpb * pitch;
-				if( lane == 0 ) {
+				double * const raw0 = reinterpret_cast< double * >( dot_smem + 128 );       // [kDotStages][2][cpb][pitch]
+				double * const prod0 = raw0 + kDotStages * stage_elems;                      // [2][cpb][ppitch]
+				if( t == 0 ) {
 					for( int s = 0; s < kDotStages; ++s ) {
-						bulk::mbar_init( full + s, 1u );
+						bulk::mbar_init( full_raw + s, 1u );
+					}
+					for( int s = 0; s < 2; ++s ) {
+						bulk::mbar_init( full_prod + s, 3u );  // one arrival per converter warp
+						bulk::mbar_init( empty_prod + s, 1u ); // the adding warp
 					}
 					bulk::mbar_fence_init();
 				}
-				__syncwarp();
+				__syncthreads();
 				dep_trigger();
 				dep_wait();
 				const uint64_t nchunks = ( n + kDotChunk - 1 ) / kDotChunk;
@@ -329,91 +300,125 @@ namespace slabgpu {
 				// tiles of the block's longest chunk (its first: only the last chunk of the vector is short)
 				const uint64_t longest = n - chunk0 * kDotChunk < kDotChunk ? n - chunk0 * kDotChunk : kDotChunk;
 				const int ntiles = static_cast< int >( ( longest + tile - 1 ) / tile );
-				const uint64_t begin = ( chunk0 + lane ) * kDotChunk; // this lane's chunk
-				const int len = lane < nmine ? static_cast< int >( n - begin < kDotChunk ? n - begin : kDotChunk ) : 0;
-				const bool aligned = ( ( reinterpret_cast< uintptr_t >( x ) | reinterpret_cast< uintptr_t >( y ) ) & 15 ) == 0;
-				// tile t of every chunk of the block into stage t % kDotStages: whole, 16-byte-aligned pieces by bulk copies,
-				// a ragged or unaligned piece by the lane itself (+0.0 behind the end of the vector: adding a +0.0 product to
-				// a sum that started from +0.0 changes nothing)
-				const auto issue = [ & ]( int t ) {
-					const int s = t % kDotStages;
-					double * const xs = stage0 + s * stage_elems + static_cast< size_t >( lane ) * pitch;
-					double * const ys = xs + static_cast< size_t >( cpb ) * pitch;
-					const int have = len - t * tile < 0 ? 0 : ( len - t * tile < tile ? len - t * tile : tile );
-					const bool by_copy = aligned && have == tile;
-					unsigned int bytes = by_copy ? static_cast< unsigned int >( tile ) * 16u : 0u;
-					#pragma unroll
-					for( int o = 16; o > 0; o >>= 1 ) {
-						bytes += __shfl_xor_sync( 0xffffffffu, bytes, o );
-					}
-					if( lane < nmine && !by_copy ) {
-						for( int i = 0; i < tile; ++i ) {
-							xs[ i ] = i < have ? x[ begin + static_cast< uint64_t >( t ) * tile + i ] : 0.0;
-							ys[ i ] = i < have ? y[ begin + static_cast< uint64_t >( t ) * tile + i ] : 0.0;
+
+				if( t < 32 ) {
+					// ------------------------------------------------ the adding warp: lane c walks chunk c's products
+					double acc = 0.0;
+					#pragma unroll 1
+					for( int k = 0; k < ntiles; ++k ) {
+						const int b = k & 1;
+						bulk::mbar_wait( full_prod + b, static_cast< unsigned int >( ( k >> 1 ) & 1 ) );
+						if( lane < nmine ) {
+							acc = chain_sum( prod0 + ( static_cast< size_t >( b ) * cpb + lane ) * ppitch, tile, acc );
+						}
+						__syncwarp();
+						if( lane == 0 ) {
+							bulk::mbar_arrive( empty_prod + b );
 						}
 					}
-					__syncwarp();
-					if( lane == 0 ) {
-						if( bytes > 0u ) {
-							bulk::mbar_arrive_expect_tx( full + s, bytes );
-						} else {
-							bulk::mbar_arrive( full + s );
-						}
-					}
-					__syncwarp();
-					if( by_copy ) {
-						bulk::g2s( xs, x + begin + static_cast< uint64_t >( t ) * tile, static_cast< unsigned int >( tile ) * 8u, full + s );
-						bulk::g2s( ys, y + begin + static_cast< uint64_t >( t ) * tile, static_cast< unsigned int >( tile ) * 8u, full + s );
-					}
-				};
-				for( int t = 0; t < kDotStages - 1 && t < ntiles; ++t ) {
-					issue( t );
-				}
-				double acc = 0.0;
-				#pragma unroll 1
-				for( int t = 0; t < ntiles; ++t ) {
-					if( t + kDotStages - 1 < ntiles ) {
-						issue( t + kDotStages - 1 ); // into the stage consumed in the previous round
-					}
-					const int s = t % kDotStages;
-					bulk::mbar_wait( full + s, static_cast< unsigned int >( ( t / kDotStages ) & 1 ) );
 					if( lane < nmine ) {
-						const double * const xs = stage0 + s * stage_elems + static_cast< size_t >( lane ) * pitch;
-						acc = chain_prod( xs, xs + static_cast< size_t >( cpb ) * pitch, tile, acc );
+						partials[ chunk0 + lane ] = acc;
 					}
-					__syncwarp();
-					bulk::fence_proxy_async(); // the stage is read; the copy engine may write it again
+					__threadfence();
+				} else {
+					// ------------------------------------------------ the converter warps
+					const int ct = t - 32; // 0..95
+					const bool issuer = t < 64; // lanes of warp 1 own the copy engine: lane c <-> chunk c
+					const uint64_t begin = ( chunk0 + lane ) * kDotChunk;
+					const int len = ( issuer && lane < nmine ) ? static_cast< int >( n - begin < kDotChunk ? n - begin : kDotChunk ) : 0;
+					const bool aligned = ( ( reinterpret_cast< uintptr_t >( x ) | reinterpret_cast< uintptr_t >( y ) ) & 15 ) == 0;
+					// tile k of every chunk of the block into raw stage k % kDotStages: whole, 16-byte-aligned pieces by bulk
+					// copies, a ragged or unaligned piece by the lane itself (+0.0 behind the end of the vector: adding a +0.0
+					// product to a sum that started from +0.0 changes nothing)
+					const auto issue = [ & ]( int k ) {
+						const int s = k % kDotStages;
+						double * const xs = raw0 + s * stage_elems + static_cast< size_t >( lane ) * pitch;
+						double * const ys = xs + static_cast< size_t >( cpb ) * pitch;
+						const int have = len - k * tile < 0 ? 0 : ( len - k * tile < tile ? len - k * tile : tile );
+						const bool by_copy = aligned && have == tile;
+						unsigned int bytes = by_copy ? static_cast< unsigned int >( tile ) * 16u : 0u;
+						#pragma unroll
+						for( int o = 16; o > 0; o >>= 1 ) {
+							bytes += __shfl_xor_sync( 0xffffffffu, bytes, o );
+						}
+						if( lane < nmine && !by_copy ) {
+							for( int i = 0; i < tile; ++i ) {
+								xs[ i ] = i < have ? x[ begin + static_cast< uint64_t >( k ) * tile + i ] : 0.0;
+								ys[ i ] = i < have ? y[ begin + static_cast< uint64_t >( k ) * tile + i ] : 0.0;
+							}
+						}
+						__syncwarp();
+						if( lane == 0 ) {
+							if( bytes > 0u ) {
+								bulk::mbar_arrive_expect_tx( full_raw + s, bytes );
+							} else {
+								bulk::mbar_arrive( full_raw + s );
+							}
+						}
+						__syncwarp();
+						if( by_copy ) {
+							bulk::g2s( xs, x + begin + static_cast< uint64_t >( k ) * tile, static_cast< unsigned int >( tile ) * 8u, full_raw + s );
+							bulk::g2s( ys, y + begin + static_cast< uint64_t >( k ) * tile, static_cast< unsigned int >( tile ) * 8u, full_raw + s );
+						}
+					};
+					if( issuer ) {
+						for( int k = 0; k < kDotStages && k < ntiles; ++k ) {
+							issue( k );
+						}
+					}
+					#pragma unroll 1
+					for( int k = 0; k < ntiles; ++k ) {
+						const int s = k % kDotStages, b = k & 1;
+						bulk::mbar_wait( full_raw + s, static_cast< unsigned int >( ( k / kDotStages ) & 1 ) );
+						if( k >= 2 ) { // the adding warp is done with the product tile this one replaces
+							bulk::mbar_wait( empty_prod + b, static_cast< unsigned int >( ( ( k >> 1 ) - 1 ) & 1 ) );
+						}
+						const double * const xs = raw0 + s * stage_elems;
+						const double * const ys = xs + static_cast< size_t >( cpb ) * pitch;
+						double * const pd = prod0 + static_cast< size_t >( b ) * cpb * ppitch;
+						const int total = nmine * tile;
+						for( int idx = ct; idx < total; idx += kDotThreads - 32 ) {
+							const int c = idx / tile, i = idx - c * tile;
+							pd[ c * ppitch + i ] = __dmul_rn( xs[ c * pitch + i ], ys[ c * pitch + i ] );
+						}
+						__syncwarp();
+						if( lane == 0 ) {
+							bulk::mbar_arrive( full_prod + b );
+						}
+						// the raw stage is free once all three converter warps have read it
+						asm volatile( "bar.sync 2, 96;" ::: "memory" );
+						if( issuer && k + kDotStages < ntiles ) {
+							bulk::fence_proxy_async();
+							issue( k + kDotStages );
+						}
+					}
 				}
-				if( lane < nmine ) {
-					partials[ chunk0 + lane ] = acc;
+				__syncthreads();
+				if( t == 0 ) {
+					is_last = atomicAdd( counter, 1u ) == gridDim.x - 1;
 				}
-				__threadfence();
-				__syncwarp();
-				unsigned int ticket = 0u;
-				if( lane == 0 ) {
-					ticket = atomicAdd( counter, 1u );
-				}
-				ticket = __shfl_sync( 0xffffffffu, ticket, 0 );
-				if( ticket != gridDim.x - 1 ) {
+				__syncthreads();
+				if( !is_last ) {
 					return;
 				}
-				// the warp that finishes last adds the per-chunk partials in chunk order: a chain for lane 0, fed through
-				// shared memory in tiles that all lanes fetch together
+				// the block that finishes last adds the per-chunk partials in chunk order: a chain for thread 0, fed through
+				// shared memory in tiles that all threads fetch together
 				__threadfence();
-				const int room = static_cast< int >( kDotStages * stage_elems < 2048 ? kDotStages * stage_elems : 2048 );
+				const size_t have_doubles = kDotStages * stage_elems + static_cast< size_t >( 2 ) * cpb * ppitch;
+				const int room = static_cast< int >( have_doubles < 4096 ? have_doubles : 4096 );
 				double total = 0.0;
 				for( uint64_t t0 = 0; t0 < nchunks; t0 += room ) {
 					const int m = static_cast< int >( nchunks - t0 < static_cast< uint64_t >( room ) ? nchunks - t0 : room );
-					__syncwarp();
-					for( int i = lane; i < m; i += 32 ) {
-						stage0[ i ] = __ldcg( partials + t0 + i );
+					__syncthreads();
+					for( int i = t; i < m; i += kDotThreads ) {
+						raw0[ i ] = __ldcg( partials + t0 + i );
 					}
-					__syncwarp();
-					if( lane == 0 ) {
-						total = chain_sum( stage0, m, total );
+					__syncthreads();
+					if( t == 0 ) {
+						total = chain_sum( raw0, m, total );
 					}
 				}
-				if( lane == 0 ) {
+				if( t == 0 ) {
 					*out = total;
 					*counter = 0u;
 				}
@@ -939,17 +944,17 @@ namespace slabgpu {
 		namespace {
 			// products per chunk and stage: as long as three stages of every chunk of the block fit shared memory
 			int dot_exact_tile( int cpb ) {
-				return cpb <= 14 ? 256 : ( cpb <= 28 ? 128 : 64 );
+				return cpb <= 12 ? 256 : ( cpb <= 24 ? 128 : 64 );
 			}
 			size_t dot_exact_smem( int cpb, int tile ) {
-				return 128 + static_cast< size_t >( kDotStages ) * 2 * cpb * ( tile + 2 ) * sizeof( double );
+				return 128 + ( static_cast< size_t >( kDotStages ) * 2 * cpb * ( tile + 2 ) + static_cast< size_t >( 2 ) * cpb * ( tile + 1 ) ) * sizeof( double );
 			}
 		} // namespace
 
 		void dot_exact_prepare() { // function attributes; outside any stream capture
 			static bool done = false;
 			if( !done ) {
-				SLAB_CUDA( cudaFuncSetAttribute( k_dot_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( 200 * 1024 ) ) );
+				SLAB_CUDA( cudaFuncSetAttribute( k_dot_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast< int >( 216 * 1024 ) ) );
 				done = true;
 			}
 		}
@@ -977,7 +982,7 @@ namespace slabgpu {
 			const int tile = dot_exact_tile( cpb );
 			cudaLaunchConfig_t cfg{};
 			cfg.gridDim = dim3( grid, 1, 1 );
-			cfg.blockDim = dim3( 32, 1, 1 );
+			cfg.blockDim = dim3( kDotThreads, 1, 1 );
 			cfg.dynamicSmemBytes = dot_exact_smem( cpb, tile );
 			cfg.stream = st;
 			cudaLaunchAttribute attr[ 1 ];
