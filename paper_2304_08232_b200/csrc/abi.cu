@@ -119,6 +119,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_tile_ns = static_cast< int >( value );
 		} else if( k == "planes" ) {
 			g_use_planes = value ? 1 : 0;
+		} else if( k == "dot_tile" ) {
+			g_dot_tile = static_cast< int >( value );
 		} else if( k == "dot_cpb" ) {
 			g_dot_cpb = static_cast< int >( value );
 		} else if( k == "plane_autotune" ) {

@@ -55,6 +55,7 @@ namespace slabgpu {
 
 	extern uint64_t g_tuning_epoch;  // bumped by every slab_set_tuning: cached graphs are keyed by it
 	extern size_t g_l2_persist_bytes;
+	extern int g_dot_tile;            // exact dot: tile override (0 = automatic)
 	extern int g_dot_cpb;             // exact dot: chunks per block override (0 = automatic)
 	extern size_t g_l2_window_max;
 	extern int g_l2_window;

@@ -36,6 +36,7 @@ namespace slabgpu {
 	// L2 persisting carve-out (set by slab_ctx_create from the device limits; 0 = unused)
 	size_t g_l2_persist_bytes = 0;
 	int g_dot_cpb = 0; // exact dot: chunks per block (0 = spread the chunks over the SMs once)
+	int g_dot_tile = 0; // exact dot: products per chunk and stage (0 = automatic)
 	size_t g_l2_window_max = 0;
 	// attach an access-policy window on z to fine-level colour steps. OFF by default: measured on B200
 	// (tools/l2_window_probe.py) the carve-out helps the 192^3 sweep by 2.6% but costs 12-18% at 104^3 and
@@ -965,7 +966,7 @@ namespace slabgpu {
 				launch( k_dot_empty, 1, 1, st, out );
 				return;
 			}
-			// as many chunks per block as spread the chunks over the SMs once (at most one per lane of the adding warp)
+			// as many chunks per block as spread the chunks over the SMs (at most one per lane of the adding warp)
 			const uint64_t nchunks = ( n + kDotChunk - 1 ) / kDotChunk;
 			static int sms = 0;
 			if( sms == 0 ) {
@@ -973,13 +974,18 @@ namespace slabgpu {
 				SLAB_CUDA( cudaGetDevice( &device ) );
 				SLAB_CUDA( cudaDeviceGetAttribute( &sms, cudaDevAttrMultiProcessorCount, device ) );
 			}
-			int cpb = static_cast< int >( ( nchunks + sms - 1 ) / sms );
+			// two blocks per SM (their adding warps sit on different sub-partitions and fill each other's hand-over gaps):
+			// measured 65 against 78 us at 192^3 (tools/exact_dot_tiles.py)
+			int cpb = static_cast< int >( ( nchunks + 2 * sms - 1 ) / ( 2 * sms ) );
 			cpb = cpb < 1 ? 1 : ( cpb > 32 ? 32 : cpb );
 			if( g_dot_cpb > 0 ) {
 				cpb = g_dot_cpb > 32 ? 32 : g_dot_cpb;
 			}
 			const unsigned int grid = static_cast< unsigned int >( ( nchunks + cpb - 1 ) / cpb );
-			const int tile = dot_exact_tile( cpb );
+			int tile = dot_exact_tile( cpb );
+			if( g_dot_tile > 0 && dot_exact_smem( cpb, g_dot_tile ) <= 216 * 1024 && ( g_dot_tile % 2 ) == 0 ) {
+				tile = g_dot_tile;
+			}
 			cudaLaunchConfig_t cfg{};
 			cfg.gridDim = dim3( grid, 1, 1 );
 			cfg.blockDim = dim3( kDotThreads, 1, 1 );

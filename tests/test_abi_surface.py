@@ -103,3 +103,30 @@ def test_bench_counting_matches_survey_denominators():
     assert bench.sweep_bytes_planes((192, 192, 192)) == 52 * 192 ** 3
     assert bench.spmv_bytes_planes((256, 256, 256)) == 16 * n
     assert bench.format_bytes_per_iteration((192, 192, 192)) < bench.algorithmic_bytes_per_iteration((192, 192, 192)) / 8
+
+
+def test_reference_arm_prints_the_contract_line():
+    """bench.py --impl reference (the CPU arm the driver runs beside ours) on the smallest workload: one JSON line with the
+    contract's keys, `impl: reference`, zero copies, no kernel launches, and the same `config` object our arm prints."""
+    import json
+    import subprocess
+    import sys
+
+    import bench
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--workload", "hpcg16", "--steps", "2",
+                          "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "vs_baseline",
+                "dtype", "data", "config", "cpu_baseline", "e2e", "gpu_launches"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["metric"] == "hpcg_gflops" and line["unit"] == "GFLOP/s" and line["value"] > 0
+    assert line["higher_is_better"] is True and line["vs_baseline"] is None and line["dtype"] == "f64" and line["gpu_launches"] == 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert line["config"] == bench.workload_config("hpcg16", bench.WORKLOADS["hpcg16"], 1)  # the same object as our arm's
+    assert "note" not in line["config"]
