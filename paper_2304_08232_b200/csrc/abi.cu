@@ -125,6 +125,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_dot_cpb = static_cast< int >( value );
 		} else if( k == "plane_autotune" ) {
 			g_plane_autotune = value ? 1 : 0;
+		} else if( k == "side_rr" ) {
+			g_side_rr = value ? 1 : 0;
 		} else if( k == "fuse_rz" ) {
 			g_fuse_rz = static_cast< int >( value ); // 0 off, 1 for systems of at least 2^19 rows, 2 always
 		} else if( k == "plane_pad_lines" ) {
@@ -244,8 +246,11 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		kern::dot_exact_prepare();
 		SLAB_CUDA( cudaMalloc( &ctx->d_scalars, S_COUNT * sizeof( double ) ) );
 		SLAB_CUDA( cudaMemset( ctx->d_scalars, 0, S_COUNT * sizeof( double ) ) );
-		SLAB_CUDA( cudaMalloc( &ctx->d_counter, sizeof( unsigned int ) ) );
-		SLAB_CUDA( cudaMemset( ctx->d_counter, 0, sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaMalloc( &ctx->d_counter, 2 * sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaMemset( ctx->d_counter, 0, 2 * sizeof( unsigned int ) ) );
+		SLAB_CUDA( cudaStreamCreateWithFlags( &ctx->side_stream, cudaStreamNonBlocking ) );
+		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->side_fork, cudaEventDisableTiming ) );
+		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->side_join, cudaEventDisableTiming ) );
 		SLAB_CUDA( cudaDeviceSynchronize() ); // the memsets ran on the legacy stream
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_start ) );
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_stop ) );
@@ -277,6 +282,10 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		cudaEventDestroy( ctx->timer_stop );
 		cudaEventDestroy( ctx->solve_start );
 		cudaEventDestroy( ctx->solve_stop );
+		cudaFree( ctx->d_partials_side );
+		cudaEventDestroy( ctx->side_fork );
+		cudaEventDestroy( ctx->side_join );
+		cudaStreamDestroy( ctx->side_stream );
 		cudaStreamDestroy( ctx->stream );
 		delete ctx;
 	} );

@@ -53,7 +53,11 @@ namespace slabgpu {
 		// deferred (fixed-iteration solves on a communicator): r'r of an iteration is not reduced where it is computed
 		// but travels with the next iteration's r'z in one allreduce of two doubles — one collective less per iteration,
 		// no change to any rank's arithmetic; the history entry of iteration k-1 is written inside iteration k
-		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred ) {
+		// side_rr (fixed-iteration solves in exact-dot mode on one process): r'r is only needed for the history, and an exact
+		// dot is a chain of dependent additions that leaves the GPU almost idle — so the r'r of the PREVIOUS iteration runs
+		// on a side stream beside this iteration's V-cycle (both only read r) and is recorded one iteration late, like
+		// the deferred reduction above
+		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred, bool side_rr ) {
 			slab_ctx_s * ctx = H->ctx;
 			cudaStream_t st = ctx->stream;
 			slab_vec_s * r = ws->r.get();
@@ -61,6 +65,12 @@ namespace slabgpu {
 			slab_vec_s * p = ws->p.get();
 			slab_vec_s * q = ws->q.get();
 			bool fused_rz = false;
+			if( side_rr ) {
+				SLAB_CUDA( cudaEventRecord( ctx->side_fork, st ) );
+				SLAB_CUDA( cudaStreamWaitEvent( ctx->side_stream, ctx->side_fork, 0 ) );
+				kern::dot_exact( ctx->side_stream, r->d, r->d, H->n, ctx->d_partials_side, ctx->d_counter + 1, ctx->d_scalars + S_RR );
+				SLAB_CUDA( cudaEventRecord( ctx->side_join, ctx->side_stream ) );
+			}
 			if( cfg->use_preconditioner ) {
 				// cg.hpp:111: the V-cycle starts from z = 0. Levels that run the plane phases take that as a flag of their
 				// first phase (nothing is read, every slab is zeros) instead of a pass that writes the zeros
@@ -84,8 +94,11 @@ namespace slabgpu {
 			if( deferred ) {
 				allreduce_slots( ctx, S_RHO, 2 ); // r'z of this iteration, r'r of the one before (0 in front of the first)
 			}
+			if( side_rr ) {
+				SLAB_CUDA( cudaStreamWaitEvent( st, ctx->side_join, 0 ) ); // long done: the V-cycle is ten times the dot
+			}
 			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
-			if( deferred ) {
+			if( deferred || side_rr ) {
 				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, false );
 			}
 			if( ctx->dot_mode == SLAB_DOT_TREE ) {
@@ -108,9 +121,11 @@ namespace slabgpu {
 				op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
 				op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
 				kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
-				op_dot_to_slot( r, r, S_RR, !deferred );                              // cg.hpp:132
+				if( !side_rr ) {
+					op_dot_to_slot( r, r, S_RR, !deferred );                          // cg.hpp:132
+				}
 			}
-			if( !deferred ) {
+			if( !deferred && !side_rr ) {
 				kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
 			}
 		}
@@ -180,6 +195,19 @@ namespace slabgpu {
 		if( deferred && limit > 0 ) {
 			SLAB_CUDA( cudaMemsetAsync( ctx->d_scalars + S_RR, 0, sizeof( double ), st ) ); // nothing to add in front of the first iteration
 		}
+		const bool side_rr = fixed && !deferred && ctx->dot_mode == SLAB_DOT_EXACT && g_side_rr != 0 && !ctx->profiling && limit > 0;
+		if( side_rr ) { // scratch of the side stream's dot (never shared with the main stream's dots)
+			const uint64_t need = ( n + kDotChunk - 1 ) / kDotChunk;
+			if( need > ctx->partials_side_cap ) {
+				SLAB_CUDA( cudaStreamSynchronize( st ) );
+				SLAB_CUDA( cudaStreamSynchronize( ctx->side_stream ) );
+				cudaFree( ctx->d_partials_side );
+				ctx->d_partials_side = nullptr;
+				SLAB_CUDA( cudaMalloc( &ctx->d_partials_side, std::max< uint64_t >( need, 1024 ) * sizeof( double ) ) );
+				ctx->partials_side_cap = std::max< uint64_t >( need, 1024 );
+				++ctx->scratch_gen;
+			}
+		}
 		// iteration graph, cached per (x, config)
 		bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
@@ -192,7 +220,7 @@ namespace slabgpu {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
 				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
-				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 );
+				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 );
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -207,7 +235,7 @@ namespace slabgpu {
 				try {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 					try {
-						iteration_enqueue( H, ws, x, cfg, deferred );
+						iteration_enqueue( H, ws, x, cfg, deferred, side_rr );
 					} catch( ... ) {
 						cudaStreamEndCapture( st, &graph );
 						if( graph ) {
@@ -263,7 +291,7 @@ namespace slabgpu {
 					ws->key_fused = ctx->fused_transfers;
 					ws->key_epoch = g_tuning_epoch;
 					ws->key_scratch = ctx->scratch_gen;
-					ws->key_deferred = deferred ? 1 : 0;
+					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 );
 				}
 			}
 		}
@@ -273,7 +301,7 @@ namespace slabgpu {
 				SLAB_CUDA( cudaGraphLaunch( ws->iter_exec, st ) );
 				count_launch( ws->iter_launches );
 			} else {
-				iteration_enqueue( H, ws, x, cfg, deferred );
+				iteration_enqueue( H, ws, x, cfg, deferred, side_rr );
 			}
 			if( cfg->use_preconditioner ) {
 				vcycle_stats_all( H, cfg->sweeps );
@@ -287,6 +315,10 @@ namespace slabgpu {
 			}
 			if( deferred && limit > 0 ) { // the last iteration's r'r is still this rank's part
 				allreduce_slot( ctx, S_RR );
+				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, true );
+			}
+			if( side_rr ) { // the last iteration's r'r has not been taken yet
+				op_dot_to_slot( ws->r.get(), ws->r.get(), S_RR );
 				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, true );
 			}
 			if( limit > 0 ) {

@@ -84,6 +84,7 @@ namespace slabgpu {
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
 	extern int g_plane_autotune;      // plane.cu: measure proposed tile shapes at level creation (default 1)
+	extern int g_side_rr;             // cg.cu: exact-dot mode, r'r on a side stream beside the next V-cycle (default 1)
 	extern int g_fuse_rz;             // cg.cu: r'z on the last plane phases of the V-cycle in tree-dot mode (default 1)
 	extern int g_plane_pad_lines;     // plane.cu: pad lines to a divisor of 32 threads (0 never, 1 up to 35 % idle, 2 always)
 	extern int g_plane_warp_sync;     // plane.cu: warp instead of block barriers between the x-parity colours of a line (default 1)
@@ -210,7 +211,12 @@ struct slab_ctx_s {
 	double * d_partials = nullptr;  // reduction scratch
 	uint64_t partials_cap = 0;
 	uint64_t scratch_gen = 0;       // bumped whenever d_partials moves: part of every cached graph's key
-	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting)
+	unsigned int * d_counter = nullptr; // "last block done" tickets (zeroed, self-resetting); [1] belongs to the side stream
+	// exact-dot solves: r'r (needed for the history only) runs on a side stream beside the next V-cycle (cg.cu)
+	cudaStream_t side_stream = nullptr;
+	cudaEvent_t side_fork = nullptr, side_join = nullptr;
+	double * d_partials_side = nullptr;
+	uint64_t partials_side_cap = 0;
 	double * h_pinned = nullptr;    // pinned staging for scalar read-back
 	uint64_t h_pinned_cap = 0;
 	cudaEvent_t timer_start = nullptr, timer_stop = nullptr; // slab_ctx_timer_* (caller-owned interval)
