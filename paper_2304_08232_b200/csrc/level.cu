@@ -184,7 +184,8 @@ namespace slabgpu {
 			if( ctx->dist == nullptr && D.n_ghost == 0 && L->colorA.packed.usable() && ( D.l[ 0 ] % 2 ) == 0
 				&& box_tile_lattice_ok( ctx, L->d_rows, L->color_pos, D ) ) {
 				box_tile_build( ctx, L->colorA, L->d_rows, D, L->tile );
-				if( L->tile.usable() && kern::gs_planes_usable( L->tile, 0, ctx->sm_count ) ) {
+				// (whether a level of this size takes the plane phases is decided per call, planes_usable: here only whether it could)
+				if( L->tile.usable() && kern::gs_planes_usable( L->tile, std::numeric_limits< int64_t >::max(), ctx->sm_count ) ) {
 					L->planes_ok = true;
 					L->zs.reset( vec_new( ctx, L->n, 0.0 ) );
 					kern::gs_planes_prepare();
