@@ -75,7 +75,10 @@ int slab_set_programmatic_launch( int enabled );
 /* performance knobs that never change results: "stream_rows" (launches with at least this many rows
  * use the streaming kernel shape), "stream_variant" (which streaming shape), "pdl", "halo_overlap" (boundary
  * rows first, halo messages beside the interior rows), "l2_window"; "planes" / "plane_min_rows" / "plane_ty" /
- * "plane_cz" / "plane_ns" (plane-phase smoother of regular box levels, csrc/plane.cu) and "spmv_planes" /
+ * "plane_cz" / "plane_ns" / "plane_autotune" (levels time the tile shapes their cost models propose when they are built) /
+ * "plane_warp_sync" / "plane_pad_lines" (plane-phase smoother of regular box levels, csrc/plane.cu), "fuse_rz" (tree-dot
+ * mode: r'z on the last plane phases of the V-cycle), "side_rr" (exact-dot mode: r'r on a side stream), "dot_cpb" /
+ * "dot_tile" (shape of the exact dot) and "spmv_planes" /
  * "spmv_plane_min_rows" / "spmv_plane_ty" / "spmv_plane_cz" / "spmv_plane_ns" (slab-staged product, csrc/plane_spmv.cu); for the dictionary-coded matrix copy: "packed" (use it, default 1),
  * "pack_build" (build it when a matrix is created, default 1), "keep_plain" (default 1; 0 frees the plain arrays of
  * matrices created afterwards whose coded copy has no escaped rows — 32 instead of 324 bytes per 27-point row, at the
