@@ -141,19 +141,21 @@ def spmv_bytes_planes(dims):
 
 
 def format_bytes_per_iteration(dims, levels=LEVELS):
-    """compulsory bytes of one CG iteration in the formats the kernels actually read: matrix-free
-    plane sweeps (52 n per symmetric sweep) and products (16 n), the fused transfers (16 n_c out, 8 n_c in), and on
-    the finest level set_all(z) 8n, r'z 16n, the p update 24n and the fused x/r update + r'r 48n."""
+    """compulsory bytes of one CG iteration (tree-dot mode) in the formats the kernels actually read:
+    matrix-free plane sweeps (52 n per symmetric sweep; the first sweep of a V-cycle starts from a zero guess that is a
+    flag, not a vector: 8 n less) and products (16 n), the fused transfers (16 n_c out, 8 n_c in), and on the finest
+    level the p update 24 n and the fused x/r update + r'r 48 n; r'z rides on the last plane phases (nothing extra) from
+    2^19 rows on, below that it is its own pass over r and z (16 n)."""
     ld = level_dims(dims, levels)
     total = 0
     for k, d in enumerate(ld):
         n = d[0] * d[1] * d[2]
         last = k == len(ld) - 1 and levels > 1
-        total += (1 if last else 2) * sweep_bytes_planes(d)
+        total += (1 if last else 2) * sweep_bytes_planes(d) - 8 * n
         if not last and levels > 1:
             total += 24 * (n // 8)
         if k == 0:
-            total += spmv_bytes_planes(d) + (8 + 16 + 24 + 48) * n
+            total += spmv_bytes_planes(d) + (24 + 48) * n + (0 if n >= (1 << 19) else 16 * n)
     return total
 
 
@@ -551,7 +553,8 @@ def main():
             "model_bytes_per_iteration": iter_bytes,
             "model_frac": iter_bytes * CG_ITERS / (ms_per_step * 1e-3) / 1e9 / peak,
             "what": "format_*: the bytes one iteration has to move in the formats the kernels read (matrix-free plane "
-                    "sweeps and products); model_*: SURVEY §8d's fused-minimum model with 12 B per stored nonzero, which "
+                    "sweeps and products, the zero initial guess of a V-cycle as a flag, r'z fused into the last plane "
+                    "phases); model_*: SURVEY §8d's fused-minimum model with 12 B per stored nonzero, which "
                     "a matrix-free format exceeds by construction (kept for comparison with matrix-streaming codes)",
         },
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(main_run["launches"]),
