@@ -77,7 +77,9 @@ int slab_set_programmatic_launch( int enabled );
  * rows first, halo messages beside the interior rows), "l2_window"; "planes" / "plane_min_rows" / "plane_ty" /
  * "plane_cz" / "plane_ns" / "plane_autotune" (levels time the tile shapes their cost models propose when they are built) /
  * "plane_warp_sync" / "plane_pad_lines" (plane-phase smoother of regular box levels, csrc/plane.cu), "fuse_rz" (tree-dot
- * mode: r'z on the last plane phases of the V-cycle), "side_rr" (exact-dot mode: r'r on a side stream), "dot_cpb" /
+ * mode: r'z on the last plane phases of the V-cycle), "side_rr" (exact-dot mode: r'r on a side stream), "lazy_x" (fixed-iteration
+ * solves take the x update one iteration late on a low-priority stream under the coarse levels of the next V-cycle: 0 off,
+ * 1 for systems of at least 2^20 rows, 2 always; "lazy_x_prio", "lazy_x_blocks" shape that pass), "dot_cpb" /
  * "dot_tile" (shape of the exact dot) and "spmv_planes" /
  * "spmv_plane_min_rows" / "spmv_plane_ty" / "spmv_plane_cz" / "spmv_plane_ns" (slab-staged product, csrc/plane_spmv.cu); for the dictionary-coded matrix copy: "packed" (use it, default 1),
  * "pack_build" (build it when a matrix is created, default 1), "keep_plain" (default 1; 0 frees the plain arrays of
@@ -88,6 +90,9 @@ int slab_set_programmatic_launch( int enabled );
  * rows, a thread-block cluster up to 4096, which is an experiment that does not pay; 0 = per-colour launches; env SLAB_CLUSTER_ROWS). Process-wide; each also has an environment variable
  * SLAB_<KEY> for the first four packed keys and the older ones. */
 int slab_set_tuning( const char * key, int64_t value );
+/* Environment only: SLAB_PLANE_TUNE_CACHE=<file> keeps the tile shapes the plane phases measured ("lx ly lz phase ty cz
+ * ns" per line) and re-uses them in later processes — a run and a profiler's run of it then execute the same shapes;
+ * SLAB_PLANE_DEBUG=1 prints the shapes. */
 
 /* ------------------------------------------------------------------ context */
 int slab_ctx_create( int device, slab_ctx_t * out );

@@ -125,6 +125,12 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_dot_cpb = static_cast< int >( value );
 		} else if( k == "plane_autotune" ) {
 			g_plane_autotune = value ? 1 : 0;
+		} else if( k == "lazy_x" ) {
+			g_lazy_x = static_cast< int >( value ); // 0 off, 1 for systems of at least 2^20 rows, 2 always
+		} else if( k == "lazy_x_prio" ) {
+			g_lazy_x_prio = value ? 1 : 0;
+		} else if( k == "lazy_x_blocks" ) {
+			g_lazy_x_blocks = static_cast< int >( value );
 		} else if( k == "side_rr" ) {
 			g_side_rr = value ? 1 : 0;
 		} else if( k == "fuse_rz" ) {
@@ -242,7 +248,11 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		ctx->cc_major = prop.major;
 		ctx->cc_minor = prop.minor;
 		ctx->hbm_bytes = prop.totalGlobalMem;
-		SLAB_CUDA( cudaStreamCreateWithFlags( &ctx->stream, cudaStreamNonBlocking ) );
+		{
+			int least = 0, greatest = 0; // the main stream above the lazy-x stream (created below with the least priority)
+			SLAB_CUDA( cudaDeviceGetStreamPriorityRange( &least, &greatest ) );
+			SLAB_CUDA( cudaStreamCreateWithPriority( &ctx->stream, cudaStreamNonBlocking, greatest ) );
+		}
 		kern::dot_exact_prepare();
 		SLAB_CUDA( cudaMalloc( &ctx->d_scalars, S_COUNT * sizeof( double ) ) );
 		SLAB_CUDA( cudaMemset( ctx->d_scalars, 0, S_COUNT * sizeof( double ) ) );
@@ -251,6 +261,13 @@ int slab_ctx_create( int device, slab_ctx_t * out ) {
 		SLAB_CUDA( cudaStreamCreateWithFlags( &ctx->side_stream, cudaStreamNonBlocking ) );
 		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->side_fork, cudaEventDisableTiming ) );
 		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->side_join, cudaEventDisableTiming ) );
+		{
+			int least = 0, greatest = 0;
+			SLAB_CUDA( cudaDeviceGetStreamPriorityRange( &least, &greatest ) );
+			SLAB_CUDA( cudaStreamCreateWithPriority( &ctx->lazy_stream, cudaStreamNonBlocking, least ) );
+		}
+		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->lazy_fork, cudaEventDisableTiming ) );
+		SLAB_CUDA( cudaEventCreateWithFlags( &ctx->lazy_join, cudaEventDisableTiming ) );
 		SLAB_CUDA( cudaDeviceSynchronize() ); // the memsets ran on the legacy stream
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_start ) );
 		SLAB_CUDA( cudaEventCreate( &ctx->timer_stop ) );
@@ -286,6 +303,9 @@ int slab_ctx_destroy( slab_ctx_t ctx ) {
 		cudaEventDestroy( ctx->side_fork );
 		cudaEventDestroy( ctx->side_join );
 		cudaStreamDestroy( ctx->side_stream );
+		cudaEventDestroy( ctx->lazy_fork );
+		cudaEventDestroy( ctx->lazy_join );
+		cudaStreamDestroy( ctx->lazy_stream );
 		cudaStreamDestroy( ctx->stream );
 		delete ctx;
 	} );

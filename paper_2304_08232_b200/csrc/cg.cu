@@ -57,7 +57,13 @@ namespace slabgpu {
 		// dot is a chain of dependent additions that leaves the GPU almost idle — so the r'r of the PREVIOUS iteration runs
 		// on a side stream beside this iteration's V-cycle (both only read r) and is recorded one iteration late, like
 		// the deferred reduction above
-		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred, bool side_rr ) {
+		// lazy_x (fixed-iteration solves on one process): nothing inside an iteration reads x, and p keeps its value until
+		// the next p update — so cg.hpp:128 of iteration k-1 runs inside iteration k, on a low-priority stream that the
+		// V-cycle forks after the finest level's pre-smoother: the pass (24 n bytes) streams under the coarse levels, which
+		// are latency-bound and leave HBM idle. The r update leaves alpha in S_ALPHA; the last iteration's x update
+		// follows the loop. Same operations on the same operands: x has the same bits.
+		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred, bool side_rr,
+			bool lazy_x ) {
 			slab_ctx_s * ctx = H->ctx;
 			cudaStream_t st = ctx->stream;
 			slab_vec_s * r = ws->r.get();
@@ -70,6 +76,16 @@ namespace slabgpu {
 				SLAB_CUDA( cudaStreamWaitEvent( ctx->side_stream, ctx->side_fork, 0 ) );
 				kern::dot_exact( ctx->side_stream, r->d, r->d, H->n, ctx->d_partials_side, ctx->d_counter + 1, ctx->d_scalars + S_RR );
 				SLAB_CUDA( cudaEventRecord( ctx->side_join, ctx->side_stream ) );
+			}
+			const auto fork_x = [ ctx, st, x, p, ws, H ]() {
+				SLAB_CUDA( cudaEventRecord( ctx->lazy_fork, st ) );
+				SLAB_CUDA( cudaStreamWaitEvent( ctx->lazy_stream, ctx->lazy_fork, 0 ) );
+				kern::cg_update_x( ctx->lazy_stream, x->d, p->d, ctx->d_scalars, ws->d_iter, H->n, ctx->sm_count );
+				SLAB_CUDA( cudaEventRecord( ctx->lazy_join, ctx->lazy_stream ) );
+			};
+			ctx->after_presmooth = nullptr;
+			if( lazy_x ) {
+				ctx->after_presmooth = fork_x;
 			}
 			if( cfg->use_preconditioner ) {
 				// cg.hpp:111: the V-cycle starts from z = 0. Levels that run the plane phases take that as a flag of their
@@ -86,6 +102,12 @@ namespace slabgpu {
 			} else {
 				op_waxpby( z, 1.0, r, 0.0, r ); // cg.hpp:114
 			}
+			if( lazy_x ) {
+				if( ctx->after_presmooth ) { // no level took it (no preconditioner, a one-level hierarchy, unfused transfers)
+					ctx->after_presmooth = nullptr;
+					fork_x();
+				}
+			}
 			if( fused_rz ) {
 				kern::sum_partials( st, ctx->d_partials, mg_vcycle_rz_partials( H ), ctx->d_scalars + S_RHO );
 			} else {
@@ -96,6 +118,9 @@ namespace slabgpu {
 			}
 			if( side_rr ) {
 				SLAB_CUDA( cudaStreamWaitEvent( st, ctx->side_join, 0 ) ); // long done: the V-cycle is ten times the dot
+			}
+			if( lazy_x ) {
+				SLAB_CUDA( cudaStreamWaitEvent( st, ctx->lazy_join, 0 ) ); // the pending x update read p
 			}
 			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
 			if( deferred || side_rr ) {
@@ -112,7 +137,7 @@ namespace slabgpu {
 						static_cast< int64_t >( H->n ), ctx->d_partials, ctx->d_counter, ctx->d_scalars + S_PQ ); // cg.hpp:122-123
 				}
 				allreduce_slot( ctx, S_PQ );
-				kern::cg_update_xr_dot( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
+				kern::cg_update_xr_dot( st, lazy_x ? nullptr : x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
 					ctx->d_counter );                                                 // cg.hpp:127-132
 				if( !deferred ) {
 					allreduce_slot( ctx, S_RR );
@@ -120,7 +145,7 @@ namespace slabgpu {
 			} else {
 				op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
 				op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
-				kern::cg_update_xr( st, x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
+				kern::cg_update_xr( st, lazy_x ? nullptr : x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
 				if( !side_rr ) {
 					op_dot_to_slot( r, r, S_RR, !deferred );                          // cg.hpp:132
 				}
@@ -208,6 +233,8 @@ namespace slabgpu {
 				++ctx->scratch_gen;
 			}
 		}
+		const bool lazy_x = fixed && !halo_has_comm( ctx ) && g_lazy_x != 0 && !ctx->profiling && limit > 0
+			&& ( g_lazy_x >= 2 || n >= ( uint64_t( 1 ) << 20 ) ); // below that the extra launch and the fork/join cost more than the pass
 		// iteration graph, cached per (x, config)
 		bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
@@ -220,7 +247,7 @@ namespace slabgpu {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
 				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
-				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 );
+				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 );
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -235,7 +262,7 @@ namespace slabgpu {
 				try {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 					try {
-						iteration_enqueue( H, ws, x, cfg, deferred, side_rr );
+						iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
 					} catch( ... ) {
 						cudaStreamEndCapture( st, &graph );
 						if( graph ) {
@@ -246,7 +273,8 @@ namespace slabgpu {
 					}
 					SLAB_CUDA( cudaStreamEndCapture( st, &graph ) );
 					ws->iter_launches = thread_launches() - before;
-					const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph, 0 );
+					const cudaError_t err = cudaGraphInstantiate( &ws->iter_exec, graph,
+						lazy_x && g_lazy_x_prio != 0 ? cudaGraphInstantiateFlagUseNodePriority : 0 ); // the x pass yields to the V-cycle
 					cudaGraphDestroy( graph );
 					SLAB_CUDA( err );
 					captured = true;
@@ -291,7 +319,7 @@ namespace slabgpu {
 					ws->key_fused = ctx->fused_transfers;
 					ws->key_epoch = g_tuning_epoch;
 					ws->key_scratch = ctx->scratch_gen;
-					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 );
+					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 );
 				}
 			}
 		}
@@ -301,7 +329,7 @@ namespace slabgpu {
 				SLAB_CUDA( cudaGraphLaunch( ws->iter_exec, st ) );
 				count_launch( ws->iter_launches );
 			} else {
-				iteration_enqueue( H, ws, x, cfg, deferred, side_rr );
+				iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
 			}
 			if( cfg->use_preconditioner ) {
 				vcycle_stats_all( H, cfg->sweeps );
@@ -320,6 +348,9 @@ namespace slabgpu {
 			if( side_rr ) { // the last iteration's r'r has not been taken yet
 				op_dot_to_slot( ws->r.get(), ws->r.get(), S_RR );
 				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, true );
+			}
+			if( lazy_x ) { // the last iteration's x update is still pending (the iteration counter is past 0 here)
+				kern::cg_update_x( st, x->d, ws->p->d, ctx->d_scalars, ws->d_iter, n, 0 );
 			}
 			if( limit > 0 ) {
 				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ws->d_hist_rr, limit * sizeof( double ), cudaMemcpyDeviceToHost,

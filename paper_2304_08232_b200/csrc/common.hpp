@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -84,6 +85,9 @@ namespace slabgpu {
 	extern int g_spmv_plane_ty, g_spmv_plane_cz, g_spmv_plane_ns; // shape overrides (0 = automatic)
 	extern int g_plane_unit;          // plane.cu: additions of -e where every off-diagonal value is -1.0 (default 1)
 	extern int g_plane_autotune;      // plane.cu: measure proposed tile shapes at level creation (default 1)
+	extern int g_lazy_x;              // cg.cu: fixed-iteration solves take cg.hpp:128 one iteration late, on a side stream under the coarse levels of the next V-cycle (default 1)
+	extern int g_lazy_x_prio;         // ... the iteration graph runs its nodes with the priorities of the streams they were captured on (default 1)
+	extern int g_lazy_x_blocks;       // ... blocks per SM of that pass (default 1)
 	extern int g_side_rr;             // cg.cu: exact-dot mode, r'r on a side stream beside the next V-cycle (default 1)
 	extern int g_fuse_rz;             // cg.cu: r'z on the last plane phases of the V-cycle in tree-dot mode (default 1)
 	extern int g_plane_pad_lines;     // plane.cu: pad lines to a divisor of 32 threads (0 never, 1 up to 35 % idle, 2 always)
@@ -105,7 +109,7 @@ namespace slabgpu {
 	// device scalar slots used by the CG driver (doubles in ctx->d_scalars)
 	// S_RHO and S_RR are neighbours: on a communicator r'z of an iteration and r'r of the one before travel in ONE
 	// allreduce of two doubles (cg.cu)
-	enum Scalar { S_RHO = 0, S_RR, S_RHO_PREV, S_PQ, S_TMP, S_BB, S_COUNT = 16 };
+	enum Scalar { S_RHO = 0, S_RR, S_RHO_PREV, S_PQ, S_TMP, S_BB, S_ALPHA, S_COUNT = 16 };
 
 	// Dictionary-coded companion of a SELL matrix (packed.cu). Every stored entry is replaced by one
 	// byte: the index of its (column - row, value) pair in a dictionary of at most 254 pairs found in
@@ -215,6 +219,11 @@ struct slab_ctx_s {
 	// exact-dot solves: r'r (needed for the history only) runs on a side stream beside the next V-cycle (cg.cu)
 	cudaStream_t side_stream = nullptr;
 	cudaEvent_t side_fork = nullptr, side_join = nullptr;
+	// lazy x (cg.cu): the x update of the previous iteration on its own low-priority stream, forked by the V-cycle after
+	// the finest level's pre-smoother (level.cu takes `after_presmooth` once)
+	cudaStream_t lazy_stream = nullptr;
+	cudaEvent_t lazy_fork = nullptr, lazy_join = nullptr;
+	std::function< void() > after_presmooth;
 	double * d_partials_side = nullptr;
 	uint64_t partials_side_cap = 0;
 	double * h_pinned = nullptr;    // pinned staging for scalar read-back

@@ -831,15 +831,20 @@ namespace slabgpu {
 				const double rho = scalars[ S_RHO ];
 				const double alpha = __ddiv_rn( rho, scalars[ S_PQ ] ); // cg.hpp:127
 				if( i < n ) {
-					x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );  // cg.hpp:128
+					if( x != nullptr ) { // else: cg.hpp:128 is taken later by k_cg_update_x (cg.cu, lazy x)
+						x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );  // cg.hpp:128
+					}
 					r[ i ] = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -alpha, q[ i ] ) ); // cg.hpp:129
 				}
 				if( i == 0 ) {
 					scalars[ S_RHO_PREV ] = rho; // cg.hpp:130 (nobody reads rho_prev in this launch)
+					scalars[ S_ALPHA ] = alpha;
 				}
 			}
 
 			// the same update with r'r (cg.hpp:132) reduced in the tree-dot shape on the way out
+			// WITH_X false: cg.hpp:128 is taken later by k_cg_update_x (cg.cu, lazy x)
+			template< bool WITH_X >
 			__global__ void __launch_bounds__( kBlock ) k_cg_update_xr_dot( double * x, double * r, const double * p,
 				const double * q, double * scalars, uint64_t n, double * partials, unsigned int * counter ) {
 				__shared__ double smem[ 32 ];
@@ -853,23 +858,28 @@ namespace slabgpu {
 				const uint64_t pairs = n >> 1;
 				double acc1 = 0.0;
 				for( uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x; i < pairs; i += stride ) {
-					const double2 xv = reinterpret_cast< const double2 * >( x )[ i ];
-					const double2 pv = reinterpret_cast< const double2 * >( p )[ i ];
+					if( WITH_X ) {
+						const double2 xv = reinterpret_cast< const double2 * >( x )[ i ];
+						const double2 pv = reinterpret_cast< const double2 * >( p )[ i ];
+						double2 xn;
+						xn.x = __dadd_rn( __dmul_rn( 1.0, xv.x ), __dmul_rn( alpha, pv.x ) );
+						xn.y = __dadd_rn( __dmul_rn( 1.0, xv.y ), __dmul_rn( alpha, pv.y ) );
+						reinterpret_cast< double2 * >( x )[ i ] = xn;
+					}
 					const double2 rv = reinterpret_cast< const double2 * >( r )[ i ];
 					const double2 qv = reinterpret_cast< const double2 * >( q )[ i ];
-					double2 xn, rn;
-					xn.x = __dadd_rn( __dmul_rn( 1.0, xv.x ), __dmul_rn( alpha, pv.x ) );
-					xn.y = __dadd_rn( __dmul_rn( 1.0, xv.y ), __dmul_rn( alpha, pv.y ) );
+					double2 rn;
 					rn.x = __dadd_rn( __dmul_rn( 1.0, rv.x ), __dmul_rn( -alpha, qv.x ) );
 					rn.y = __dadd_rn( __dmul_rn( 1.0, rv.y ), __dmul_rn( -alpha, qv.y ) );
-					reinterpret_cast< double2 * >( x )[ i ] = xn;
 					reinterpret_cast< double2 * >( r )[ i ] = rn;
 					acc = __dadd_rn( acc, __dmul_rn( rn.x, rn.x ) );
 					acc1 = __dadd_rn( acc1, __dmul_rn( rn.y, rn.y ) );
 				}
 				if( blockIdx.x == 0 && threadIdx.x == 0 && ( n & 1 ) ) {
 					const uint64_t i = n - 1;
-					x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );
+					if( WITH_X ) {
+						x[ i ] = __dadd_rn( __dmul_rn( 1.0, x[ i ] ), __dmul_rn( alpha, p[ i ] ) );
+					}
 					const double rn = __dadd_rn( __dmul_rn( 1.0, r[ i ] ), __dmul_rn( -alpha, q[ i ] ) );
 					r[ i ] = rn;
 					acc1 = __dadd_rn( acc1, __dmul_rn( rn, rn ) );
@@ -877,8 +887,54 @@ namespace slabgpu {
 				acc = __dadd_rn( acc, acc1 );
 				if( blockIdx.x == 0 && threadIdx.x == 0 ) {
 					scalars[ S_RHO_PREV ] = rho;
+					scalars[ S_ALPHA ] = alpha;
 				}
 				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, scalars + S_RR, smem, &is_last );
+			}
+
+			// cg.hpp:128 of the PREVIOUS iteration (cg.cu, lazy x): x <- x + alpha p with the alpha that iteration's r update
+			// left in S_ALPHA. Nothing inside an iteration reads x, and p keeps its value until the next p update, so this
+			// pass runs on a side stream under the latency-bound coarse levels of the next V-cycle. A small grid with
+			// four 16-byte loads per array in flight per thread: enough for a third of the HBM rate, few enough blocks to
+			// leave the SMs to the V-cycle. The first iteration has nothing pending.
+			__global__ void __launch_bounds__( kBlock ) k_cg_update_x( double * x, const double * p, const double * scalars,
+				const unsigned int * iter_counter, uint64_t n ) {
+				dep_trigger();
+				dep_wait();
+				if( *iter_counter == 0u ) {
+					return;
+				}
+				const double alpha = scalars[ S_ALPHA ];
+				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
+				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
+				const uint64_t pairs = n >> 1;
+				double2 * const x2 = reinterpret_cast< double2 * >( x );
+				const double2 * const p2 = reinterpret_cast< const double2 * >( p );
+				uint64_t i = tid;
+				for( ; i + 3 * stride < pairs; i += 4 * stride ) {
+					double2 xv[ 4 ], pv[ 4 ];
+					#pragma unroll
+					for( int k = 0; k < 4; ++k ) {
+						xv[ k ] = x2[ i + k * stride ];
+						pv[ k ] = p2[ i + k * stride ];
+					}
+					#pragma unroll
+					for( int k = 0; k < 4; ++k ) {
+						xv[ k ].x = __dadd_rn( __dmul_rn( 1.0, xv[ k ].x ), __dmul_rn( alpha, pv[ k ].x ) );
+						xv[ k ].y = __dadd_rn( __dmul_rn( 1.0, xv[ k ].y ), __dmul_rn( alpha, pv[ k ].y ) );
+						x2[ i + k * stride ] = xv[ k ];
+					}
+				}
+				for( ; i < pairs; i += stride ) {
+					double2 xv = x2[ i ];
+					const double2 pv = p2[ i ];
+					xv.x = __dadd_rn( __dmul_rn( 1.0, xv.x ), __dmul_rn( alpha, pv.x ) );
+					xv.y = __dadd_rn( __dmul_rn( 1.0, xv.y ), __dmul_rn( alpha, pv.y ) );
+					x2[ i ] = xv;
+				}
+				if( tid == 0 && ( n & 1 ) ) {
+					x[ n - 1 ] = __dadd_rn( __dmul_rn( 1.0, x[ n - 1 ] ), __dmul_rn( alpha, p[ n - 1 ] ) );
+				}
 			}
 
 			__global__ void k_cg_record( const double * scalars, double * hist_rr, double * hist_pq,
@@ -1194,9 +1250,26 @@ namespace slabgpu {
 			launch( k_cg_update_xr, n == 0 ? 1u : blocks_for( n ), kBlock, st, x, r, p, q, scalars, n );
 		}
 
+		void cg_update_x( cudaStream_t st, double * x, const double * p, const double * scalars, const unsigned int * iter_counter,
+			uint64_t n, int sm_count ) {
+			if( n == 0 ) {
+				return;
+			}
+			const uint64_t pairs = ( n + 1 ) >> 1;
+			const uint64_t want = ( pairs + kBlock * 4 - 1 ) / ( kBlock * 4 );
+			const uint64_t cap = static_cast< uint64_t >( sm_count > 0 ? sm_count : 148 ) * ( g_lazy_x_blocks > 0 ? g_lazy_x_blocks : 1 );
+			launch( k_cg_update_x, static_cast< unsigned int >( want < 1 ? 1 : ( want > cap ? cap : want ) ), kBlock, st, x, p, scalars,
+				iter_counter, n );
+		}
+
 		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n, int sm_count, double * partials, unsigned int * counter ) {
-			launch( k_cg_update_xr_dot, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
+			if( x == nullptr ) {
+				launch( k_cg_update_xr_dot< false >, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
+					scalars, n, partials, counter );
+				return;
+			}
+			launch( k_cg_update_xr_dot< true >, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
 				scalars, n, partials, counter );
 		}
 

@@ -111,12 +111,16 @@ namespace slabgpu {
 		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,
 			const unsigned int * iter_counter, uint64_t n );
-		// alpha = rho/pq; x = 1*x + alpha*p; r = 1*r + (-alpha)*q; rho_prev <- rho
+		// alpha = rho/pq; x = 1*x + alpha*p; r = 1*r + (-alpha)*q; rho_prev <- rho, S_ALPHA <- alpha
+		// x == nullptr (both shapes): the x update is left to cg_update_x
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n );
 		// the same plus r'r -> scalars[S_RR] (cg.hpp:132) in the tree-dot shape; partials: dot_tree_blocks doubles
 		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
 			uint64_t n, int sm_count, double * partials, unsigned int * counter );
+		// x = 1*x + scalars[S_ALPHA]*p unless *iter_counter == 0 (cg.hpp:128 one iteration late, cg.cu lazy x)
+		void cg_update_x( cudaStream_t st, double * x, const double * p, const double * scalars, const unsigned int * iter_counter,
+			uint64_t n, int sm_count );
 		// hist_rr[it] = rr, hist_pq[it] = pq, ++it
 		// iteration k-1's bookkeeping inside iteration k (it > 0 only; last: after the final iteration, no increment)
 		void cg_record_deferred( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq, unsigned int * iter_counter, bool last );

@@ -701,6 +701,11 @@ namespace slabgpu {
 			for( uint64_t sweep = 0; sweep < sweeps; ++sweep ) {
 				sweep_pair_enqueue( L, z, r, sweep == 0 && zero_guess && planes_usable( L ) ? 8 : 0, sweep + 1 == sweeps && fuse_residual ? 2 : 0 );
 			}
+			if( ctx->after_presmooth ) { // cg.cu: side work that belongs under the coarse levels (taken once, by the finest level)
+				std::function< void() > side;
+				side.swap( ctx->after_presmooth );
+				side();
+			}
 			if( !fuse_residual ) {
 				kern::residual_restrict( ctx->stream, L->colorA, L->d_rows,
 					static_cast< int64_t >( L->r_c->n ), z->d, r->d, L->r_c->d, L->z_c->d );
@@ -726,6 +731,7 @@ namespace slabgpu {
 			fail( SLAB_ERR_INVALID_ARGUMENT, "SmootherConfig: sweeps must be at least 1" );
 		}
 		slab_ctx_s * ctx = L->ctx;
+		ctx->after_presmooth = nullptr; // only cg.cu hands the V-cycle side work (a solve that threw may have left it behind)
 		mg_vcycle_prepare( L, z, r, sweeps ); // allocations and uploads happen before any capture
 		if( !ctx->use_graphs || ctx->profiling ) {
 			halo_exchange( L, z, -1 ); // the caller's z: ghost copies may be stale

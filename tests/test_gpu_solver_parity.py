@@ -261,3 +261,45 @@ def test_host_entry_point_rejects_unusable_output_buffers(slab, ctx):
         slab.cg_solve_host(h, b, np.zeros(n), cfg, out=frozen)
     with pytest.raises(slab.DimensionMismatch):
         slab.cg_solve_host(h, np.ones(n + 1), np.zeros(n + 1), cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,levels", [((16, 16, 16), 4), ((5, 7, 9), 1), ((24, 16, 40), 3)])
+def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dims, levels):
+    """cg.hpp:128 taken one iteration late on a side stream under the coarse levels of the next V-cycle (cg.cu, lazy x):
+    the solution and the history have the bits of the in-place order and of the oracle, in both dot modes, with and
+    without the iteration graph, preconditioned or not, and for 1, 2 and 50 iterations (the first iteration has nothing
+    pending, the last update follows the loop)"""
+    from paper_2304_08232_b200 import _capi
+
+    h = ctx.build_hierarchy(dims, levels)
+    n = h.n()
+    b, _ = ctx.random_vector(n, 7)
+    x0, _ = ctx.random_vector(n, 11)
+    oh = oracle.build_hierarchy(*dims, levels)
+    try:
+        for iters in (1, 2, 50):
+            for precond in (True, False):
+                cfg = slab.CGConfig(max_iters=iters, fixed_iterations=iters, use_preconditioner=precond)
+                ctx.dot_mode = slab.DOT_EXACT
+                ores = oracle.cg_solve(oh, b.values(), x0.values(), max_iters=iters, fixed_iterations=iters, use_preconditioner=precond)
+                for mode in (slab.DOT_EXACT, slab.DOT_TREE):
+                    ctx.dot_mode = mode
+                    got = {}
+                    for lazy in (2, 0):
+                        for graphs in (1, 0):
+                            _capi.set_tuning("lazy_x", lazy)
+                            ctx.set_graphs(bool(graphs))
+                            res = slab.cg_solve(h, b, x0, cfg)
+                            got[(lazy, graphs)] = (res.solution.values().copy(), list(res.residual_history))
+                    base = got[(0, 1)]
+                    for key, (sol, hist) in got.items():
+                        assert np.array_equal(sol, base[0]), (iters, precond, mode, key)
+                        assert hist == base[1], (iters, precond, mode, key)
+                    if mode == slab.DOT_EXACT:
+                        assert np.array_equal(base[0], ores.solution)
+                        assert base[1] == list(ores.residual_history)
+    finally:
+        _capi.set_tuning("lazy_x", 1)
+        ctx.set_graphs(True)
+        ctx.dot_mode = slab.DOT_EXACT
