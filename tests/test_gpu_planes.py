@@ -167,3 +167,57 @@ def test_fused_rz_dot_and_zero_guess_keep_the_history(slab, ctx, tuning):
         ctx.dot_mode = slab.DOT_EXACT
     assert np.max(np.abs(got[2] - got[0]) / got[0]) <= 1e-12
     assert np.max(np.abs(got[2] - want) / want) <= 1e-10
+
+
+def test_zero_numerators_take_the_fast_path_with_the_right_sign(slab, ctx, oracle, tuning):
+    """(+-0) / d without the division's slow path (plane.cu, divide): right-hand sides and guesses that are zero or
+    negative zero over most of the box — the benchmark's b = A 1 is zero away from the faces — give the bits of the
+    per-colour kernels and of the oracle, signs of the zeros included"""
+    dims = (12, 10, 8)
+    n = dims[0] * dims[1] * dims[2]
+    rng = np.random.default_rng(11)
+    lvl = ctx.build_hierarchy(dims, 1)
+    olvl = oracle.build_hierarchy(*dims, 1)
+    cases = []
+    for zfill, rfill in ((0.0, 0.0), (-0.0, -0.0), (0.0, -0.0), (-0.0, 0.0)):
+        z0 = np.full(n, zfill)
+        r = np.full(n, rfill)
+        cases.append((z0.copy(), r.copy()))
+        hot = rng.integers(0, n, 5)
+        z0[hot] = rng.standard_normal(5)
+        r[rng.integers(0, n, 5)] = rng.standard_normal(5)
+        cases.append((z0, r))
+    for z0, r in cases:
+        got = {}
+        for on in (1, 0):
+            tuning(planes=on)
+            z = ctx.DenseVector(z0)
+            slab.rbgs_symmetric(lvl, z, ctx.DenseVector(r))
+            got[on] = z.values()
+        want = oracle.rbgs_symmetric(olvl, z0, r)
+        assert np.array_equal(got[1].view(np.uint64), got[0].view(np.uint64))
+        assert np.array_equal(got[1].view(np.uint64), np.asarray(want).view(np.uint64))
+
+
+def test_tile_shape_cache_file_round_trip(slab, ctx, oracle, tuning, tmp_path, monkeypatch):
+    """SLAB_PLANE_TUNE_CACHE: the shapes a level measured are appended to the file and re-used by the next level of the
+    same box (a profiler's run then executes the measured shapes); results do not depend on it"""
+    path = tmp_path / "shapes.txt"
+    monkeypatch.setenv("SLAB_PLANE_TUNE_CACHE", str(path))
+    dims = (32, 24, 16)
+    n = dims[0] * dims[1] * dims[2]
+    buf, _ = oracle.random_vector(2 * n, 5)
+    r, z0 = buf[:n], buf[n:]
+    want = oracle.rbgs_symmetric(oracle.build_hierarchy(*dims, 1), z0, r)
+    lines = None
+    for _ in range(2):
+        lvl = ctx.build_hierarchy(dims, 1)
+        z = ctx.DenseVector(z0)
+        slab.rbgs_symmetric(lvl, z, ctx.DenseVector(r))
+        assert np.array_equal(z.values(), want)
+        text = path.read_text().splitlines() if path.exists() else []
+        if lines is None:
+            lines = text
+            assert 1 <= len(lines) <= 3 and all(len(l.split()) == 7 and l.startswith("32 24 16 ") for l in lines)
+        else:
+            assert text == lines  # the second build read its shapes, measured nothing, wrote nothing
