@@ -235,6 +235,18 @@ namespace slabgpu {
 		}
 		const bool lazy_x = fixed && !halo_has_comm( ctx ) && g_lazy_x != 0 && !ctx->profiling && limit > 0
 			&& ( g_lazy_x >= 2 || n >= ( uint64_t( 1 ) << 20 ) ); // below that the extra launch and the fork/join cost more than the pass
+		// several iterations per graph launch (fixed-iteration solves on one process): the hand-over from one
+		// iteration's last kernel to the next one's first is then a programmatic edge inside a graph instead of the gap
+		// between two graph launches. The largest divisor of the iteration count up to the knob.
+		uint64_t batch = 1;
+		if( fixed && !halo_has_comm( ctx ) && g_iter_batch > 1 ) {
+			for( uint64_t k = std::min< uint64_t >( limit, static_cast< uint64_t >( g_iter_batch ) ); k > 1; --k ) {
+				if( limit % k == 0 ) {
+					batch = k;
+					break;
+				}
+			}
+		}
 		// iteration graph, cached per (x, config)
 		bool graphs = ctx->use_graphs != 0 && !ctx->profiling; // timing instrumentation needs plain launches
 		if( cfg->use_preconditioner && limit > 0 ) {
@@ -247,7 +259,7 @@ namespace slabgpu {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
 				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
-				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 );
+				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 ) || ws->key_batch != batch;
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -262,7 +274,9 @@ namespace slabgpu {
 				try {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 					try {
-						iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+						for( uint64_t k = 0; k < batch; ++k ) {
+							iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+						}
 					} catch( ... ) {
 						cudaStreamEndCapture( st, &graph );
 						if( graph ) {
@@ -320,26 +334,32 @@ namespace slabgpu {
 					ws->key_epoch = g_tuning_epoch;
 					ws->key_scratch = ctx->scratch_gen;
 					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 );
+					ws->key_batch = batch;
 				}
 			}
 		}
 
-		const auto run_iteration = [ & ]() {
+		// `count` iterations: the graph holds `batch` of them
+		const auto run_iterations = [ & ]( uint64_t count ) {
 			if( graphs ) {
 				SLAB_CUDA( cudaGraphLaunch( ws->iter_exec, st ) );
 				count_launch( ws->iter_launches );
 			} else {
-				iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+				for( uint64_t k = 0; k < count; ++k ) {
+					iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+				}
 			}
 			if( cfg->use_preconditioner ) {
-				vcycle_stats_all( H, cfg->sweeps );
+				for( uint64_t k = 0; k < count; ++k ) {
+					vcycle_stats_all( H, cfg->sweeps );
+				}
 			}
 		};
 
 		int breakdown = 0;
 		if( fixed ) {
-			for( uint64_t iter = 1; iter <= limit; ++iter ) {
-				run_iteration();
+			for( uint64_t iter = 0; iter < limit; iter += batch ) {
+				run_iterations( batch );
 			}
 			if( deferred && limit > 0 ) { // the last iteration's r'r is still this rank's part
 				allreduce_slot( ctx, S_RR );
@@ -370,7 +390,7 @@ namespace slabgpu {
 			}
 		} else {
 			for( uint64_t iter = 1; iter <= limit; ++iter ) {
-				run_iteration();
+				run_iterations( 1 );
 				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ctx->d_scalars + S_RR, sizeof( double ), cudaMemcpyDeviceToHost,
 					st ) );
 				SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + 1, ctx->d_scalars + S_PQ, sizeof( double ),

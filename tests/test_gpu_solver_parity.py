@@ -268,8 +268,8 @@ def test_host_entry_point_rejects_unusable_output_buffers(slab, ctx):
 def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dims, levels):
     """cg.hpp:128 taken one iteration late on a side stream under the coarse levels of the next V-cycle (cg.cu, lazy x):
     the solution and the history have the bits of the in-place order and of the oracle, in both dot modes, with and
-    without the iteration graph, preconditioned or not, and for 1, 2 and 50 iterations (the first iteration has nothing
-    pending, the last update follows the loop)"""
+    without the iteration graph, with one and with all iterations per graph launch (cg.cu, iter_batch), preconditioned or
+    not, and for 1, 2 and 50 iterations (the first iteration has nothing pending, the last update follows the loop)"""
     from paper_2304_08232_b200 import _capi
 
     h = ctx.build_hierarchy(dims, levels)
@@ -286,13 +286,13 @@ def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dim
                 for mode in (slab.DOT_EXACT, slab.DOT_TREE):
                     ctx.dot_mode = mode
                     got = {}
-                    for lazy in (2, 0):
-                        for graphs in (1, 0):
-                            _capi.set_tuning("lazy_x", lazy)
-                            ctx.set_graphs(bool(graphs))
-                            res = slab.cg_solve(h, b, x0, cfg)
-                            got[(lazy, graphs)] = (res.solution.values().copy(), list(res.residual_history))
-                    base = got[(0, 1)]
+                    for lazy, graphs, batch in ((2, 1, 50), (2, 1, 1), (2, 0, 1), (0, 1, 50), (0, 1, 1), (0, 0, 1)):
+                        _capi.set_tuning("lazy_x", lazy)
+                        _capi.set_tuning("iter_batch", batch)  # iterations per graph launch
+                        ctx.set_graphs(bool(graphs))
+                        res = slab.cg_solve(h, b, x0, cfg)
+                        got[(lazy, graphs, batch)] = (res.solution.values().copy(), list(res.residual_history))
+                    base = got[(0, 1, 1)]
                     for key, (sol, hist) in got.items():
                         assert np.array_equal(sol, base[0]), (iters, precond, mode, key)
                         assert hist == base[1], (iters, precond, mode, key)
@@ -301,5 +301,6 @@ def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dim
                         assert base[1] == list(ores.residual_history)
     finally:
         _capi.set_tuning("lazy_x", 1)
+        _capi.set_tuning("iter_batch", 50)
         ctx.set_graphs(True)
         ctx.dot_mode = slab.DOT_EXACT
