@@ -80,7 +80,8 @@ int slab_set_programmatic_launch( int enabled );
  * mode: r'z on the last plane phases of the V-cycle), "side_rr" (exact-dot mode: r'r on a side stream), "lazy_x" (fixed-iteration
  * solves take the x update one iteration late on a low-priority stream under the coarse levels of the next V-cycle: 0 off,
  * 1 for systems of at least 2^20 rows, 2 always; "lazy_x_prio", "lazy_x_blocks" shape that pass), "iter_batch" (CG iterations per graph launch in
- * fixed-iteration solves: the largest divisor of the iteration count up to this, default 50), "dot_cpb" /
+ * fixed-iteration solves: the largest divisor of the iteration count up to this, default 50), "inline_record" (those solves
+ * write the history from the p update and count iterations in the r update instead of a bookkeeping launch), "dot_cpb" /
  * "dot_tile" (shape of the exact dot) and "spmv_planes" /
  * "spmv_plane_min_rows" / "spmv_plane_ty" / "spmv_plane_cz" / "spmv_plane_ns" (slab-staged product, csrc/plane_spmv.cu); for the dictionary-coded matrix copy: "packed" (use it, default 1),
  * "pack_build" (build it when a matrix is created, default 1), "keep_plain" (default 1; 0 frees the plain arrays of

@@ -129,6 +129,8 @@ int slab_set_tuning( const char * key, int64_t value ) {
 			g_lazy_x = static_cast< int >( value ); // 0 off, 1 for systems of at least 2^20 rows, 2 always
 		} else if( k == "lazy_x_prio" ) {
 			g_lazy_x_prio = value ? 1 : 0;
+		} else if( k == "inline_record" ) {
+			g_inline_record = value ? 1 : 0;
 		} else if( k == "iter_batch" ) {
 			g_iter_batch = static_cast< int >( value );
 		} else if( k == "lazy_x_blocks" ) {

@@ -63,7 +63,7 @@ namespace slabgpu {
 		// are latency-bound and leave HBM idle. The r update leaves alpha in S_ALPHA; the last iteration's x update
 		// follows the loop. Same operations on the same operands: x has the same bits.
 		void iteration_enqueue( slab_level_s * H, CgWorkspace * ws, slab_vec_s * x, const slab_cg_config * cfg, bool deferred, bool side_rr,
-			bool lazy_x ) {
+			bool lazy_x, bool inline_record ) {
 			slab_ctx_s * ctx = H->ctx;
 			cudaStream_t st = ctx->stream;
 			slab_vec_s * r = ws->r.get();
@@ -122,8 +122,12 @@ namespace slabgpu {
 			if( lazy_x ) {
 				SLAB_CUDA( cudaStreamWaitEvent( st, ctx->lazy_join, 0 ) ); // the pending x update read p
 			}
-			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n ); // cg.hpp:117-121
-			if( deferred || side_rr ) {
+			// inline bookkeeping (fixed-iteration solves on one process): the p update writes the previous iteration's
+			// history entry, the r update bumps the iteration counter — no launch of its own for either; the last
+			// entry follows the loop
+			kern::cg_update_p( st, p->d, z->d, ctx->d_scalars, ws->d_iter, H->n, inline_record ? ws->d_hist_rr : nullptr,
+				ws->d_hist_pq );                                                      // cg.hpp:117-121
+			if( ( deferred || side_rr ) && !inline_record ) {
 				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, false );
 			}
 			if( ctx->dot_mode == SLAB_DOT_TREE ) {
@@ -138,19 +142,19 @@ namespace slabgpu {
 				}
 				allreduce_slot( ctx, S_PQ );
 				kern::cg_update_xr_dot( st, lazy_x ? nullptr : x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, ctx->sm_count, ctx->d_partials,
-					ctx->d_counter );                                                 // cg.hpp:127-132
+					ctx->d_counter, inline_record ? ws->d_iter : nullptr );           // cg.hpp:127-132
 				if( !deferred ) {
 					allreduce_slot( ctx, S_RR );
 				}
 			} else {
 				op_mxv( q, nullptr, H->A.get(), p, SLAB_DESC_NONE );                  // cg.hpp:122
 				op_dot_to_slot( p, q, S_PQ );                                         // cg.hpp:123
-				kern::cg_update_xr( st, lazy_x ? nullptr : x->d, r->d, p->d, q->d, ctx->d_scalars, H->n ); // cg.hpp:127-130
+				kern::cg_update_xr( st, lazy_x ? nullptr : x->d, r->d, p->d, q->d, ctx->d_scalars, H->n, inline_record ? ws->d_iter : nullptr ); // cg.hpp:127-130
 				if( !side_rr ) {
 					op_dot_to_slot( r, r, S_RR, !deferred );                          // cg.hpp:132
 				}
 			}
-			if( !deferred && !side_rr ) {
+			if( !deferred && !side_rr && !inline_record ) {
 				kern::cg_record( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter );
 			}
 		}
@@ -233,6 +237,7 @@ namespace slabgpu {
 				++ctx->scratch_gen;
 			}
 		}
+		const bool inline_record = fixed && !deferred && !halo_has_comm( ctx ) && g_inline_record != 0 && limit > 0;
 		const bool lazy_x = fixed && !halo_has_comm( ctx ) && g_lazy_x != 0 && !ctx->profiling && limit > 0
 			&& ( g_lazy_x >= 2 || n >= ( uint64_t( 1 ) << 20 ) ); // below that the extra launch and the fork/join cost more than the pass
 		// several iterations per graph launch (fixed-iteration solves on one process): the hand-over from one
@@ -259,7 +264,7 @@ namespace slabgpu {
 			const bool stale = ws->iter_exec == nullptr || ws->key_x != x->d || ws->key_sweeps != cfg->sweeps
 				|| ws->key_precond != cfg->use_preconditioner || ws->key_dot != ctx->dot_mode
 				|| ws->key_fused != ctx->fused_transfers || ws->key_epoch != g_tuning_epoch
-				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 ) || ws->key_batch != batch;
+				|| ws->key_scratch != ctx->scratch_gen || ws->key_deferred != ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 ) + ( inline_record ? 8 : 0 ) || ws->key_batch != batch;
 			if( stale ) {
 				if( ws->iter_exec ) {
 					cudaGraphExecDestroy( ws->iter_exec );
@@ -275,7 +280,7 @@ namespace slabgpu {
 					SLAB_CUDA( cudaStreamBeginCapture( st, halo_has_comm( ctx ) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal ) );
 					try {
 						for( uint64_t k = 0; k < batch; ++k ) {
-							iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+							iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x, inline_record );
 						}
 					} catch( ... ) {
 						cudaStreamEndCapture( st, &graph );
@@ -333,7 +338,7 @@ namespace slabgpu {
 					ws->key_fused = ctx->fused_transfers;
 					ws->key_epoch = g_tuning_epoch;
 					ws->key_scratch = ctx->scratch_gen;
-					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 );
+					ws->key_deferred = ( deferred ? 1 : 0 ) + ( side_rr ? 2 : 0 ) + ( lazy_x ? 4 : 0 ) + ( inline_record ? 8 : 0 );
 					ws->key_batch = batch;
 				}
 			}
@@ -346,7 +351,7 @@ namespace slabgpu {
 				count_launch( ws->iter_launches );
 			} else {
 				for( uint64_t k = 0; k < count; ++k ) {
-					iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x );
+					iteration_enqueue( H, ws, x, cfg, deferred, side_rr, lazy_x, inline_record );
 				}
 			}
 			if( cfg->use_preconditioner ) {
@@ -367,6 +372,8 @@ namespace slabgpu {
 			}
 			if( side_rr ) { // the last iteration's r'r has not been taken yet
 				op_dot_to_slot( ws->r.get(), ws->r.get(), S_RR );
+			}
+			if( side_rr || inline_record ) { // ... and its history entry has not been written
 				kern::cg_record_deferred( st, ctx->d_scalars, ws->d_hist_rr, ws->d_hist_pq, ws->d_iter, true );
 			}
 			if( lazy_x ) { // the last iteration's x update is still pending (the iteration counter is past 0 here)

@@ -88,6 +88,7 @@ namespace slabgpu {
 	extern int g_lazy_x;              // cg.cu: fixed-iteration solves take cg.hpp:128 one iteration late, on a side stream under the coarse levels of the next V-cycle (default 1)
 	extern int g_lazy_x_prio;         // ... the iteration graph runs its nodes with the priorities of the streams they were captured on (default 1)
 	extern int g_iter_batch;          // cg.cu: CG iterations per graph launch in fixed-iteration solves (the largest divisor of the count up to this; default 50)
+	extern int g_inline_record;       // cg.cu: the history entry and the iteration count ride on the p and r updates (default 1)
 	extern int g_lazy_x_blocks;       // ... blocks per SM of that pass (default 1)
 	extern int g_side_rr;             // cg.cu: exact-dot mode, r'r on a side stream beside the next V-cycle (default 1)
 	extern int g_fuse_rz;             // cg.cu: r'z on the last plane phases of the V-cycle in tree-dot mode (default 1)

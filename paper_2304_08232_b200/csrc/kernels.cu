@@ -799,14 +799,22 @@ namespace slabgpu {
 
 			// ------------------------------------------------------------ CG updates
 
+			// hist_rr != nullptr (cg.cu, inline bookkeeping): thread 0 also writes the PREVIOUS iteration's history entry —
+			// r'r and p'Ap still hold its values here — and the r update of this iteration bumps the counter, so no
+			// launch is spent on bookkeeping
 			__global__ void __launch_bounds__( kBlock ) k_cg_update_p( double * p, const double * z,
-				const double * scalars, const unsigned int * iter_counter, uint64_t n ) {
+				const double * scalars, const unsigned int * iter_counter, uint64_t n, double * hist_rr, double * hist_pq ) {
 				dep_trigger();
 				dep_wait();
 				const uint64_t tid = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
 				const uint64_t stride = static_cast< uint64_t >( gridDim.x ) * blockDim.x;
 				const uint64_t pairs = n >> 1;
-				const bool first = *iter_counter == 0u;
+				const unsigned int it = *iter_counter;
+				const bool first = it == 0u;
+				if( hist_rr != nullptr && tid == 0 && it > 0u ) {
+					hist_rr[ it - 1u ] = scalars[ S_RR ];
+					hist_pq[ it - 1u ] = scalars[ S_PQ ];
+				}
 				// cg.hpp:118  waxpby( p, 1.0, z, 0.0, z )  /  cg.hpp:120  waxpby( p, 1.0, z, rho / rho_prev, p )
 				const double beta = first ? 0.0 : __ddiv_rn( scalars[ S_RHO ], scalars[ S_RHO_PREV ] );
 				for( uint64_t i = tid; i < pairs; i += stride ) {
@@ -824,7 +832,7 @@ namespace slabgpu {
 			}
 
 			__global__ void k_cg_update_xr( double * x, double * r, const double * p,
-				const double * q, double * scalars, uint64_t n ) {
+				const double * q, double * scalars, uint64_t n, unsigned int * bump ) {
 				dep_trigger();
 				dep_wait();
 				const uint64_t i = static_cast< uint64_t >( blockIdx.x ) * blockDim.x + threadIdx.x;
@@ -839,6 +847,9 @@ namespace slabgpu {
 				if( i == 0 ) {
 					scalars[ S_RHO_PREV ] = rho; // cg.hpp:130 (nobody reads rho_prev in this launch)
 					scalars[ S_ALPHA ] = alpha;
+					if( bump != nullptr ) {
+						*bump += 1u; // the iteration counter (nobody reads it in this launch)
+					}
 				}
 			}
 
@@ -846,7 +857,7 @@ namespace slabgpu {
 			// WITH_X false: cg.hpp:128 is taken later by k_cg_update_x (cg.cu, lazy x)
 			template< bool WITH_X >
 			__global__ void __launch_bounds__( kBlock ) k_cg_update_xr_dot( double * x, double * r, const double * p,
-				const double * q, double * scalars, uint64_t n, double * partials, unsigned int * counter ) {
+				const double * q, double * scalars, uint64_t n, double * partials, unsigned int * counter, unsigned int * bump ) {
 				__shared__ double smem[ 32 ];
 				__shared__ bool is_last;
 				dep_trigger();
@@ -888,6 +899,9 @@ namespace slabgpu {
 				if( blockIdx.x == 0 && threadIdx.x == 0 ) {
 					scalars[ S_RHO_PREV ] = rho;
 					scalars[ S_ALPHA ] = alpha;
+					if( bump != nullptr ) {
+						*bump += 1u;
+					}
 				}
 				grid_tree_finish( block_tree_sum( acc, smem ), partials, counter, scalars + S_RR, smem, &is_last );
 			}
@@ -1238,16 +1252,13 @@ namespace slabgpu {
 		}
 
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,
-			const unsigned int * iter_counter, uint64_t n ) {
-			if( n == 0 ) {
-				return;
-			}
-			launch( k_cg_update_p, vector_grid( n ), kBlock, st, p, z, scalars, iter_counter, n );
+			const unsigned int * iter_counter, uint64_t n, double * hist_rr, double * hist_pq ) {
+			launch( k_cg_update_p, n == 0 ? 1u : vector_grid( n ), kBlock, st, p, z, scalars, iter_counter, n, hist_rr, hist_pq );
 		}
 
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
-			uint64_t n ) {
-			launch( k_cg_update_xr, n == 0 ? 1u : blocks_for( n ), kBlock, st, x, r, p, q, scalars, n );
+			uint64_t n, unsigned int * bump ) {
+			launch( k_cg_update_xr, n == 0 ? 1u : blocks_for( n ), kBlock, st, x, r, p, q, scalars, n, bump );
 		}
 
 		void cg_update_x( cudaStream_t st, double * x, const double * p, const double * scalars, const unsigned int * iter_counter,
@@ -1263,14 +1274,14 @@ namespace slabgpu {
 		}
 
 		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
-			uint64_t n, int sm_count, double * partials, unsigned int * counter ) {
+			uint64_t n, int sm_count, double * partials, unsigned int * counter, unsigned int * bump ) {
 			if( x == nullptr ) {
 				launch( k_cg_update_xr_dot< false >, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
-					scalars, n, partials, counter );
+					scalars, n, partials, counter, bump );
 				return;
 			}
 			launch( k_cg_update_xr_dot< true >, static_cast< unsigned int >( dot_tree_blocks( n, sm_count ) ), kBlock, st, x, r, p, q,
-				scalars, n, partials, counter );
+				scalars, n, partials, counter, bump );
 		}
 
 		void cg_record( cudaStream_t st, const double * scalars, double * hist_rr, double * hist_pq,

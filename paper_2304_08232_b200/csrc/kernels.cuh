@@ -109,15 +109,17 @@ namespace slabgpu {
 
 		// ---- CG vector updates with device-resident scalars (cg.hpp:116-132)
 		// p = 1*z + (rho/rho_prev)*p   (when *iter_counter == 0: p = 1*z + 0*z)
+		// hist_rr != nullptr: also hist_rr/pq[it - 1] = the previous iteration's r'r / p'Ap (it > 0)
 		void cg_update_p( cudaStream_t st, double * p, const double * z, const double * scalars,
-			const unsigned int * iter_counter, uint64_t n );
+			const unsigned int * iter_counter, uint64_t n, double * hist_rr = nullptr, double * hist_pq = nullptr );
 		// alpha = rho/pq; x = 1*x + alpha*p; r = 1*r + (-alpha)*q; rho_prev <- rho, S_ALPHA <- alpha
 		// x == nullptr (both shapes): the x update is left to cg_update_x
+		// bump != nullptr (both shapes): ++*bump (the iteration counter, with the history written by cg_update_p)
 		void cg_update_xr( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
-			uint64_t n );
+			uint64_t n, unsigned int * bump = nullptr );
 		// the same plus r'r -> scalars[S_RR] (cg.hpp:132) in the tree-dot shape; partials: dot_tree_blocks doubles
 		void cg_update_xr_dot( cudaStream_t st, double * x, double * r, const double * p, const double * q, double * scalars,
-			uint64_t n, int sm_count, double * partials, unsigned int * counter );
+			uint64_t n, int sm_count, double * partials, unsigned int * counter, unsigned int * bump = nullptr );
 		// x = 1*x + scalars[S_ALPHA]*p unless *iter_counter == 0 (cg.hpp:128 one iteration late, cg.cu lazy x)
 		void cg_update_x( cudaStream_t st, double * x, const double * p, const double * scalars, const unsigned int * iter_counter,
 			uint64_t n, int sm_count );

@@ -289,6 +289,7 @@ def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dim
                     for lazy, graphs, batch in ((2, 1, 50), (2, 1, 1), (2, 0, 1), (0, 1, 50), (0, 1, 1), (0, 0, 1)):
                         _capi.set_tuning("lazy_x", lazy)
                         _capi.set_tuning("iter_batch", batch)  # iterations per graph launch
+                        _capi.set_tuning("inline_record", 1 if lazy else 0)  # bookkeeping on the p and r updates
                         ctx.set_graphs(bool(graphs))
                         res = slab.cg_solve(h, b, x0, cfg)
                         got[(lazy, graphs, batch)] = (res.solution.values().copy(), list(res.residual_history))
@@ -302,5 +303,6 @@ def test_lazy_x_update_keeps_solution_and_history_bitwise(slab, ctx, oracle, dim
     finally:
         _capi.set_tuning("lazy_x", 1)
         _capi.set_tuning("iter_batch", 50)
+        _capi.set_tuning("inline_record", 1)
         ctx.set_graphs(True)
         ctx.dot_mode = slab.DOT_EXACT

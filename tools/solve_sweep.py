@@ -24,7 +24,7 @@ from paper_2304_08232_b200 import _capi  # noqa: E402
 
 DEFAULTS = {"packed": 1, "packed_block": 256, "packed_batch": 2, "packed_min_rows": 65536, "packed_rows": 2, "packed_rows_spmv": 3, "packed_multi_min_rows": 300000, "cluster_rows": 384,
             "stream_rows": 200000, "stream_variant": 2, "pdl": 1, "planes": 1, "plane_ty": 0, "plane_cz": 0, "plane_ns": 0, "plane_rows": 0,
-            "plane_min_rows": 0, "plane_warp_sync": 1, "plane_pad_lines": 1, "fuse_rz": 1, "side_rr": 1, "lazy_x": 1, "iter_batch": 50, "lazy_x_blocks": 1, "lazy_x_prio": 1, "spmv_planes": 1, "spmv_plane_ty": 0, "spmv_plane_cz": 0, "spmv_plane_ns": 0, "tile": 1}
+            "plane_min_rows": 0, "plane_warp_sync": 1, "plane_pad_lines": 1, "fuse_rz": 1, "side_rr": 1, "lazy_x": 1, "iter_batch": 50, "inline_record": 1, "lazy_x_blocks": 1, "lazy_x_prio": 1, "spmv_planes": 1, "spmv_plane_ty": 0, "spmv_plane_cz": 0, "spmv_plane_ns": 0, "tile": 1}
 
 
 def main():
