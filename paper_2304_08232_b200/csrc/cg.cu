@@ -206,15 +206,26 @@ namespace slabgpu {
 		op_dot_to_slot( r, r, S_RR );                        // cg.hpp:100
 		SLAB_CUDA( cudaMemsetAsync( ws->d_iter, 0, sizeof( unsigned int ), st ) );
 		ensure_pinned( ctx, 2 * ( planned + 1 ) + 2 );
-		SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned, ctx->d_scalars + S_RR, sizeof( double ), cudaMemcpyDeviceToHost, st ) );
-		SLAB_CUDA( cudaMemcpyAsync( ctx->h_pinned + 1, ctx->d_scalars + S_BB, sizeof( double ), cudaMemcpyDeviceToHost,
-			st ) );
-		SLAB_CUDA( cudaStreamSynchronize( st ) );
-		const double b_norm = std::sqrt( ctx->h_pinned[ 1 ] );
-		const double denom = b_norm > 0.0 ? b_norm : 1.0;
-		double r_norm = std::sqrt( ctx->h_pinned[ 0 ] );
+		// the two initial norms land behind the history's staging area. A tolerance-driven solve needs them on the host
+		// before its first iteration (cg.hpp:103); a fixed-iteration solve reads them with the history at the end, so
+		// that nothing waits between the prologue and the iterations: the host enqueues the iteration graph while the
+		// prologue (or, from host buffers, the upload) is still running
+		double * const h_init = ctx->h_pinned + 2 * ( planned + 1 );
+		SLAB_CUDA( cudaMemcpyAsync( h_init, ctx->d_scalars + S_RR, sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+		SLAB_CUDA( cudaMemcpyAsync( h_init + 1, ctx->d_scalars + S_BB, sizeof( double ), cudaMemcpyDeviceToHost, st ) );
+		const bool early_sync = !fixed || halo_has_comm( ctx );
+		double denom = 1.0, r_norm = 0.0;
 		uint64_t count = 0;
-		history[ count++ ] = r_norm;
+		const auto take_initial_norms = [ & ]() {
+			const double b_norm = std::sqrt( h_init[ 1 ] );
+			denom = b_norm > 0.0 ? b_norm : 1.0;
+			r_norm = std::sqrt( h_init[ 0 ] );
+			history[ count++ ] = r_norm;
+		};
+		if( early_sync ) {
+			SLAB_CUDA( cudaStreamSynchronize( st ) );
+			take_initial_norms();
+		}
 
 		const bool already_converged = !fixed && r_norm / denom < cfg->rtol; // cg.hpp:103
 		const uint64_t limit = already_converged ? 0 : planned;
@@ -387,6 +398,9 @@ namespace slabgpu {
 			}
 			SLAB_CUDA( cudaEventRecord( ctx->solve_stop, st ) );
 			SLAB_CUDA( cudaStreamSynchronize( st ) );
+			if( !early_sync ) {
+				take_initial_norms();
+			}
 			for( uint64_t k = 0; k < limit; ++k ) {
 				if( ctx->h_pinned[ limit + k ] <= 0.0 ) { // cg.hpp:124-126
 					breakdown = 1;
